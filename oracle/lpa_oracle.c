@@ -1,0 +1,574 @@
+/*
+ * lpa_oracle.c -- CPU restatement of the reference's sequential label
+ * propagation (sketchlpa 0.1.0).  TEST INFRASTRUCTURE ONLY.
+ *
+ * This file is the parity checker for the CUDA product path.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference arm
+ * may load it.  The product (paper_2411_19901_b200/) never links or calls it.
+ *
+ * Every function restates one reference function literally, in the same
+ * arithmetic (IEEE binary64 for sketch values, exactly like Python floats):
+ *
+ *   mg_accumulate      sketch.py:47-74   (first key match incl. stale keys,
+ *                                         else first value==0.0 slot, else
+ *                                         clamp-decrement every slot)
+ *   mg_merge           sketch.py:76-91   (replay non-empty slots ascending)
+ *   mg_max_key         sketch.py:93-105  (max value, ties -> smaller key)
+ *   mg_rescan_add      sketch.py:113-126
+ *   bm_accumulate      sketch.py:147-162
+ *   reduce_votes       sketch.py:165-181
+ *   chunk_bounds       lpa.py:110-118
+ *   select_label_exact lpa.py:92-107     (np.bincount order: per-label sums
+ *                                         in adjacency order, argmax = first)
+ *   select_label_bm    lpa.py:121-150
+ *   select_label_mg    lpa.py:153-193
+ *   process_vertices   lpa.py:204-224
+ *   lpa_move           lpa.py:227-241    (worker_count == 0 path only)
+ *   lpa_run            lpa.py:262-308
+ *   aux_memory_estimate lpa.py:311-333
+ *   tally / modularity metrics.py:34-74
+ *   assemble           graph.py:107-139  (canonical CSR)
+ *
+ * It also carries the synthetic graph generators (RMAT, grid, k-mer-like)
+ * whose specification DESIGN.md §6 fixes; the CUDA generators in the product
+ * must reproduce these CSR arrays bit for bit (tests/test_gen_gpu.py).
+ *
+ * Pinned against the reference's own golden vectors: tests/golden/*.npz are
+ * produced by tests/golden/make_golden.py, which imports the Python reference
+ * from /root/reference and records its outputs (tests/test_oracle.py).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#define ORC_EXACT 0
+#define ORC_BM 1
+#define ORC_MG 2
+
+typedef struct {
+    int32_t variant;          /* 0 exact, 1 bm, 2 mg  (lpa.py:51) */
+    int32_t scan_double;      /* scan_mode == "double" (lpa.py:52) */
+    int32_t sketch_slots;     /* k (lpa.py:53) */
+    int32_t pickless_gap;     /* rho (lpa.py:54) */
+    double tolerance;         /* tau (lpa.py:55) */
+    int32_t max_iterations;   /* lpa.py:56 */
+    int32_t degree_threshold; /* D_H (lpa.py:57) */
+    int32_t partial_groups;   /* R_H (lpa.py:58) */
+    int32_t shared_sketch;    /* lpa.py:60 */
+} orc_config;
+
+typedef struct {
+    int64_t n;
+    const int64_t *offsets;
+    const int32_t *targets;
+    const void *weights;
+    int32_t w_f64;
+} orc_graph;
+
+static inline double arc_w(const orc_graph *g, int64_t a) {
+    return g->w_f64 ? ((const double *)g->weights)[a] : (double)((const float *)g->weights)[a];
+}
+
+/* ------------------------------------------------------------ MG sketch */
+typedef struct {
+    int k;
+    int32_t *keys;
+    double *vals;
+} mg_t;
+
+static void mg_reset(mg_t *s) { /* MgSketch.__init__ sketch.py:34-39 */
+    for (int i = 0; i < s->k; ++i) { s->keys[i] = 0; s->vals[i] = 0.0; }
+}
+
+static void mg_accumulate(mg_t *s, int32_t key, double w) { /* sketch.py:47-74 */
+    for (int i = 0; i < s->k; ++i)
+        if (s->keys[i] == key) { s->vals[i] += w; return; }
+    for (int i = 0; i < s->k; ++i)
+        if (s->vals[i] == 0.0) { s->keys[i] = key; s->vals[i] = w; return; }
+    for (int i = 0; i < s->k; ++i) {
+        double v = s->vals[i] - w;
+        s->vals[i] = v > 0.0 ? v : 0.0;
+    }
+}
+
+static void mg_merge(mg_t *dst, const mg_t *src) { /* sketch.py:76-91 */
+    for (int i = 0; i < src->k; ++i)
+        if (src->vals[i] > 0.0) mg_accumulate(dst, src->keys[i], src->vals[i]);
+}
+
+static int mg_max_key(const mg_t *s, int32_t *out) { /* sketch.py:93-105 */
+    int found = 0;
+    int32_t best = 0;
+    double best_w = 0.0;
+    for (int i = 0; i < s->k; ++i) {
+        double v = s->vals[i];
+        if (v <= 0.0) continue;
+        int32_t c = s->keys[i];
+        if (!found || v > best_w || (v == best_w && c < best)) { best = c; best_w = v; found = 1; }
+    }
+    *out = best;
+    return found;
+}
+
+static void mg_rescan_add(mg_t *s, int32_t key, double w) { /* sketch.py:113-126 */
+    for (int i = 0; i < s->k; ++i)
+        if (s->keys[i] == key) { s->vals[i] += w; return; }
+}
+
+/* ------------------------------------------------------------ BM vote */
+typedef struct { int32_t cand; double w; } bm_t;
+
+static void bm_accumulate(bm_t *s, int32_t key, double w) { /* sketch.py:147-162 */
+    if (key == s->cand) s->w += w;
+    else if (s->w > w) s->w -= w;
+    else { s->cand = key; s->w = w; }
+}
+
+/* ------------------------------------------------------------ selectors */
+static void chunk_bounds(int64_t count, int64_t parts, int64_t r, int64_t *s, int64_t *e) {
+    /* lpa.py:110-118 */
+    int64_t base = count / parts, rem = count % parts;
+    int64_t start = r * base + (r < rem ? r : rem);
+    *s = start;
+    *e = start + base + (r < rem ? 1 : 0);
+}
+
+typedef struct {
+    mg_t *parts;   /* partial_groups sketches */
+    int32_t *kbuf;
+    double *vbuf;
+    /* exact scratch */
+    int64_t cap;
+    int64_t *idx;
+    int32_t *lab;
+    double *wt;
+} scratch_t;
+
+static void scratch_init(scratch_t *sc, const orc_config *cfg) {
+    int P = cfg->partial_groups, k = cfg->sketch_slots;
+    sc->parts = (mg_t *)malloc(sizeof(mg_t) * (size_t)P);
+    sc->kbuf = (int32_t *)malloc(sizeof(int32_t) * (size_t)P * k);
+    sc->vbuf = (double *)malloc(sizeof(double) * (size_t)P * k);
+    for (int p = 0; p < P; ++p) {
+        sc->parts[p].k = k;
+        sc->parts[p].keys = sc->kbuf + (size_t)p * k;
+        sc->parts[p].vals = sc->vbuf + (size_t)p * k;
+    }
+    sc->cap = 0; sc->idx = NULL; sc->lab = NULL; sc->wt = NULL;
+}
+
+static void scratch_free(scratch_t *sc) {
+    free(sc->parts); free(sc->kbuf); free(sc->vbuf);
+    free(sc->idx); free(sc->lab); free(sc->wt);
+}
+
+static int32_t select_mg(const orc_graph *g, const int32_t *labels, int64_t i,
+                         const orc_config *cfg, scratch_t *sc) { /* lpa.py:153-193 */
+    int64_t lo = g->offsets[i], hi = g->offsets[i + 1], deg = hi - lo;
+    int32_t cur = labels[i];
+    if (deg == 0) return cur;
+    mg_t *sk = &sc->parts[0];
+    if (deg < cfg->degree_threshold || cfg->shared_sketch) {
+        mg_reset(sk);
+        for (int64_t a = lo; a < hi; ++a) {
+            int32_t j = g->targets[a];
+            if (j != i) mg_accumulate(sk, labels[j], arc_w(g, a));
+        }
+    } else {
+        int P = cfg->partial_groups;
+        for (int p = 0; p < P; ++p) {
+            mg_t *part = &sc->parts[p];
+            mg_reset(part);
+            int64_t s, e;
+            chunk_bounds(deg, P, p, &s, &e);
+            for (int64_t t = s; t < e; ++t) {
+                int32_t j = g->targets[lo + t];
+                if (j != i) mg_accumulate(part, labels[j], arc_w(g, lo + t));
+            }
+        }
+        for (int p = 1; p < P; ++p) mg_merge(sk, &sc->parts[p]);
+    }
+    if (cfg->scan_double) {
+        for (int s = 0; s < sk->k; ++s) sk->vals[s] = 0.0; /* clear_values sketch.py:107-111 */
+        for (int64_t a = lo; a < hi; ++a) {
+            int32_t j = g->targets[a];
+            if (j != i) mg_rescan_add(sk, labels[j], arc_w(g, a));
+        }
+    }
+    int32_t best;
+    return mg_max_key(sk, &best) ? best : cur;
+}
+
+static int32_t select_bm(const orc_graph *g, const int32_t *labels, int64_t i,
+                         const orc_config *cfg) { /* lpa.py:121-150 */
+    int64_t lo = g->offsets[i], hi = g->offsets[i + 1], deg = hi - lo;
+    int32_t cur = labels[i];
+    if (deg == 0) return cur;
+    if (deg < cfg->degree_threshold) {
+        bm_t st = {cur, 0.0};
+        for (int64_t a = lo; a < hi; ++a) {
+            int32_t j = g->targets[a];
+            if (j != i) bm_accumulate(&st, labels[j], arc_w(g, a));
+        }
+        return st.cand;
+    }
+    bm_t best = {0, 0.0};
+    int P = cfg->partial_groups;
+    for (int p = 0; p < P; ++p) {
+        bm_t st = {cur, 0.0};
+        int64_t s, e;
+        chunk_bounds(deg, P, p, &s, &e);
+        for (int64_t t = s; t < e; ++t) {
+            int32_t j = g->targets[lo + t];
+            if (j != i) bm_accumulate(&st, labels[j], arc_w(g, lo + t));
+        }
+        /* reduce_votes sketch.py:165-181 */
+        if (p == 0 || st.w > best.w || (st.w == best.w && st.cand < best.cand)) best = st;
+    }
+    return best.cand;
+}
+
+static const int32_t *g_sort_lab;
+static int cmp_lab_pos(const void *pa, const void *pb) {
+    int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
+    int32_t la = g_sort_lab[a], lb = g_sort_lab[b];
+    if (la != lb) return la < lb ? -1 : 1;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+static int32_t select_exact(const orc_graph *g, const int32_t *labels, int64_t i,
+                            scratch_t *sc) { /* lpa.py:92-107 */
+    int64_t lo = g->offsets[i], hi = g->offsets[i + 1], deg = hi - lo;
+    if (deg > sc->cap) {
+        sc->cap = deg;
+        sc->idx = (int64_t *)realloc(sc->idx, sizeof(int64_t) * (size_t)deg);
+        sc->lab = (int32_t *)realloc(sc->lab, sizeof(int32_t) * (size_t)deg);
+        sc->wt = (double *)realloc(sc->wt, sizeof(double) * (size_t)deg);
+    }
+    int64_t cnt = 0;
+    for (int64_t a = lo; a < hi; ++a) {
+        int32_t j = g->targets[a];
+        if (j == i) continue;
+        sc->lab[cnt] = labels[j];
+        sc->wt[cnt] = arc_w(g, a);
+        sc->idx[cnt] = cnt;
+        ++cnt;
+    }
+    if (cnt == 0) return labels[i];
+    /* np.bincount adds weights in input order per label: stable sort by
+     * (label, position) then left-to-right sums reproduce that order. */
+    g_sort_lab = sc->lab;
+    qsort(sc->idx, (size_t)cnt, sizeof(int64_t), cmp_lab_pos);
+    int32_t best = 0;
+    double best_w = -1.0;
+    int64_t t = 0;
+    while (t < cnt) {
+        int32_t c = sc->lab[sc->idx[t]];
+        double tot = 0.0;
+        while (t < cnt && sc->lab[sc->idx[t]] == c) { tot += sc->wt[sc->idx[t]]; ++t; }
+        if (tot > best_w) { best_w = tot; best = c; } /* argmax: first (smallest) label wins ties */
+    }
+    return best;
+}
+
+static int32_t select_any(const orc_graph *g, const int32_t *labels, int64_t i,
+                          const orc_config *cfg, scratch_t *sc) { /* lpa.py:196-201 */
+    if (cfg->variant == ORC_EXACT) return select_exact(g, labels, i, sc);
+    if (cfg->variant == ORC_BM) return select_bm(g, labels, i, cfg);
+    return select_mg(g, labels, i, cfg, sc);
+}
+
+/* ------------------------------------------------------------ public API */
+int32_t orc_select(const orc_graph *g, const int32_t *labels, int64_t i, const orc_config *cfg) {
+    scratch_t sc;
+    scratch_init(&sc, cfg);
+    int32_t r = select_any(g, labels, i, cfg, &sc);
+    scratch_free(&sc);
+    return r;
+}
+
+static int64_t process_vertices(const orc_graph *g, int32_t *labels, uint8_t *unprocessed,
+                                const orc_config *cfg, int pickless, const int64_t *order,
+                                int64_t lo_pos, int64_t hi_pos, scratch_t *sc) {
+    /* lpa.py:204-224 */
+    int64_t changed = 0;
+    for (int64_t p = lo_pos; p < hi_pos; ++p) {
+        int64_t i = order ? order[p] : p;
+        if (!unprocessed[i]) continue;
+        unprocessed[i] = 0;
+        int32_t cand = select_any(g, labels, i, cfg, sc);
+        if (cand != labels[i] && (!pickless || cand < labels[i])) {
+            labels[i] = cand;
+            ++changed;
+            for (int64_t a = g->offsets[i]; a < g->offsets[i + 1]; ++a) unprocessed[g->targets[a]] = 1;
+        }
+    }
+    return changed;
+}
+
+int64_t orc_lpa_move(const orc_graph *g, int32_t *labels, uint8_t *unprocessed,
+                     const orc_config *cfg, int32_t pickless, const int64_t *order) {
+    scratch_t sc;
+    scratch_init(&sc, cfg);
+    int64_t r = process_vertices(g, labels, unprocessed, cfg, pickless, order, 0, g->n, &sc);
+    scratch_free(&sc);
+    return r;
+}
+
+/* Partial sweep over positions [lo_pos, hi_pos) -- used by bench.py's bounded
+ * CPU-baseline sample.  Same code as a full sweep. */
+int64_t orc_lpa_move_range(const orc_graph *g, int32_t *labels, uint8_t *unprocessed,
+                           const orc_config *cfg, int32_t pickless, const int64_t *order,
+                           int64_t lo_pos, int64_t hi_pos) {
+    scratch_t sc;
+    scratch_init(&sc, cfg);
+    int64_t r = process_vertices(g, labels, unprocessed, cfg, pickless, order, lo_pos, hi_pos, &sc);
+    scratch_free(&sc);
+    return r;
+}
+
+/* lpa.py:262-308.  label_hist (optional) receives the labels after each
+ * sweep (what iteration_hook sees), row-major [iteration][vertex]. */
+int32_t orc_lpa_run(const orc_graph *g, const orc_config *cfg, const int64_t *order,
+                    int32_t *labels, int64_t *delta_hist, int32_t *iters, int32_t *converged,
+                    int32_t *label_hist) {
+    int64_t n = g->n;
+    uint8_t *unprocessed = (uint8_t *)malloc((size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) { labels[i] = (int32_t)i; unprocessed[i] = 1; }
+    scratch_t sc;
+    scratch_init(&sc, cfg);
+    int32_t it, done = 0;
+    for (it = 0; it < cfg->max_iterations; ++it) {
+        int pickless = (it % cfg->pickless_gap) == 0;
+        int64_t delta = process_vertices(g, labels, unprocessed, cfg, pickless, order, 0, n, &sc);
+        delta_hist[it] = delta;
+        if (label_hist) memcpy(label_hist + (size_t)it * n, labels, sizeof(int32_t) * (size_t)n);
+        double frac = n ? (double)delta / (double)n : 0.0;
+        if (!pickless && frac < cfg->tolerance) { done = 1; ++it; break; }
+    }
+    *iters = it;
+    *converged = done;
+    scratch_free(&sc);
+    free(unprocessed);
+    return 0;
+}
+
+int64_t orc_aux_memory_estimate(int64_t n, int32_t value_bytes, const orc_config *cfg,
+                                int32_t worker_count) { /* lpa.py:311-333 */
+    int64_t workers = worker_count > 1 ? worker_count : 1;
+    int64_t base = n * (4 + 1);
+    int64_t per;
+    if (cfg->variant == ORC_EXACT) per = n * (4 + value_bytes);
+    else if (cfg->variant == ORC_MG) per = (int64_t)cfg->partial_groups * cfg->sketch_slots * (4 + value_bytes);
+    else per = (int64_t)cfg->partial_groups * (4 + value_bytes);
+    return base + workers * per;
+}
+
+/* metrics.py:34-49 (_tally).  Sums in arc order, like np.bincount. */
+int32_t orc_tally(const orc_graph *g, const int32_t *labels, int64_t *sizes,
+                  double *internal, double *incident) {
+    int64_t n = g->n;
+    for (int64_t i = 0; i < n; ++i) {
+        if (labels[i] < 0 || labels[i] >= n) return -1;
+    }
+    memset(sizes, 0, sizeof(int64_t) * (size_t)n);
+    memset(internal, 0, sizeof(double) * (size_t)n);
+    memset(incident, 0, sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t li = labels[i];
+        sizes[li] += 1;
+        for (int64_t a = g->offsets[i]; a < g->offsets[i + 1]; ++a) {
+            double w = arc_w(g, a);
+            incident[li] += w;
+            if (labels[g->targets[a]] == li) internal[li] += w;
+        }
+    }
+    return 0;
+}
+
+/* ==================================================================== */
+/*  Synthetic generators.  Counter-based, so the output   */
+/*  does not depend on thread count or device.                          */
+/* ==================================================================== */
+static inline uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+static inline uint64_t h64(uint64_t seed, uint64_t ctr) { return splitmix64(splitmix64(seed) ^ ctr); }
+
+/* Bijection on [0, 2^b). */
+static inline uint64_t perm_pow2(uint64_t x, int b, uint64_t key) {
+    if (b == 0) return 0;
+    uint64_t mask = (b >= 64) ? ~0ULL : ((1ULL << b) - 1);
+    int sh = b / 2 + 1;
+    for (int r = 0; r < 4; ++r) {
+        uint64_t k = splitmix64(key + (uint64_t)r);
+        x = (x * (k | 1ULL)) & mask;
+        if (sh < b) x ^= x >> sh;
+        x = (x + (k >> 17)) & mask;
+    }
+    return x;
+}
+static inline int ceil_log2(uint64_t n) { int b = 0; while ((1ULL << b) < n) ++b; return b; }
+/* Bijection on [0, n) by cycle walking. */
+uint64_t orc_perm(uint64_t x, uint64_t n, uint64_t key) {
+    int b = ceil_log2(n);
+    uint64_t y = perm_pow2(x, b, key);
+    while (y >= n) y = perm_pow2(y, b, key);
+    return y;
+}
+
+/* RMAT: edge e draws `scale` quadrants from 32-bit words of h64(seed, e*W+j),
+ * W = ceil(scale/2); level l uses the low word when l is even.  Quadrant
+ * A (<tA) keeps both bits 0, B sets the dst bit, C the src bit, D both.  Bit
+ * (scale-1-l) is set at level l.  Self-loops are dropped (count returned). */
+int64_t orc_rmat_edges(int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                       uint64_t seed, int32_t permute, uint64_t perm_key, uint32_t *src, uint32_t *dst) {
+    int64_t W = (scale + 1) / 2;
+    int64_t out = 0;
+    for (int64_t e = 0; e < num_edges; ++e) {
+        uint64_t u = 0, v = 0;
+        uint64_t word = 0;
+        for (int l = 0; l < scale; ++l) {
+            if ((l & 1) == 0) word = h64(seed, (uint64_t)e * (uint64_t)W + (uint64_t)(l >> 1));
+            uint32_t r = (l & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+            uint64_t bit = 1ULL << (scale - 1 - l);
+            if (r < tA) {
+            } else if (r < tAB) v |= bit;
+            else if (r < tABC) u |= bit;
+            else { u |= bit; v |= bit; }
+        }
+        if (permute) {
+            u = perm_pow2(u, scale, perm_key);
+            v = perm_pow2(v, scale, perm_key);
+        }
+        if (u == v) continue;
+        src[out] = (uint32_t)u;
+        dst[out] = (uint32_t)v;
+        ++out;
+    }
+    return out;
+}
+
+/* 2-D grid rows x cols, 4-neighbour, ids (optionally) permuted. */
+int64_t orc_grid_edges(int64_t rows, int64_t cols, int32_t permute, uint64_t perm_key,
+                       uint32_t *src, uint32_t *dst) {
+    uint64_t n = (uint64_t)rows * (uint64_t)cols;
+    int64_t out = 0;
+    for (int64_t i = 0; i < rows; ++i)
+        for (int64_t j = 0; j < cols; ++j) {
+            uint64_t v = (uint64_t)(i * cols + j);
+            uint64_t pv = permute ? orc_perm(v, n, perm_key) : v;
+            if (j + 1 < cols) {
+                uint64_t w = v + 1;
+                src[out] = (uint32_t)pv;
+                dst[out] = (uint32_t)(permute ? orc_perm(w, n, perm_key) : w);
+                ++out;
+            }
+            if (i + 1 < rows) {
+                uint64_t w = v + (uint64_t)cols;
+                src[out] = (uint32_t)pv;
+                dst[out] = (uint32_t)(permute ? orc_perm(w, n, perm_key) : w);
+                ++out;
+            }
+        }
+    return out;
+}
+
+/* k-mer-like: chain link (i,i+1) kept iff high word of h64(seed,i) < keep;
+ * n/20 chords (u,v) from h64(seed ^ 0xC0DE, c): u = low % n, v = high % n,
+ * self-loops dropped; ids permuted. */
+int64_t orc_kmer_edges(int64_t n, uint32_t keep, uint64_t seed, int32_t permute, uint64_t perm_key,
+                       uint32_t *src, uint32_t *dst) {
+    int64_t out = 0;
+    for (int64_t i = 0; i + 1 < n; ++i) {
+        uint64_t x = h64(seed, (uint64_t)i);
+        if ((uint32_t)(x >> 32) < keep) {
+            uint64_t a = (uint64_t)i, b = (uint64_t)i + 1;
+            src[out] = (uint32_t)(permute ? orc_perm(a, (uint64_t)n, perm_key) : a);
+            dst[out] = (uint32_t)(permute ? orc_perm(b, (uint64_t)n, perm_key) : b);
+            ++out;
+        }
+    }
+    int64_t chords = n / 20;
+    for (int64_t c = 0; c < chords; ++c) {
+        uint64_t x = h64(seed ^ 0xC0DEULL, (uint64_t)c);
+        uint64_t a = (uint64_t)(uint32_t)x % (uint64_t)n, b = (x >> 32) % (uint64_t)n;
+        if (a == b) continue;
+        src[out] = (uint32_t)(permute ? orc_perm(a, (uint64_t)n, perm_key) : a);
+        dst[out] = (uint32_t)(permute ? orc_perm(b, (uint64_t)n, perm_key) : b);
+        ++out;
+    }
+    return out;
+}
+
+/* ---------------------------------------------------- canonical assembly */
+static void radix_sort_u64(uint64_t *a, uint64_t *tmp, int64_t n, int bits) {
+    /* LSD radix sort, 16-bit digits, only over the low `bits` key bits. */
+    size_t *cnt = (size_t *)malloc(sizeof(size_t) * 65536);
+    uint64_t *src = a, *dstp = tmp;
+    int passes = 0;
+    for (int sh = 0; sh < bits; sh += 16) {
+        memset(cnt, 0, sizeof(size_t) * 65536);
+        for (int64_t i = 0; i < n; ++i) cnt[(src[i] >> sh) & 0xFFFF]++;
+        size_t sum = 0;
+        for (int d = 0; d < 65536; ++d) { size_t c = cnt[d]; cnt[d] = sum; sum += c; }
+        for (int64_t i = 0; i < n; ++i) dstp[cnt[(src[i] >> sh) & 0xFFFF]++] = src[i];
+        uint64_t *t = src; src = dstp; dstp = t;
+        ++passes;
+    }
+    if (passes & 1) memcpy(a, src, sizeof(uint64_t) * (size_t)n);
+    free(cnt);
+}
+
+/* graph.py:107-139 for unit-weight edge lists (every generator input has
+ * weight 1.0, so duplicate sums are exact integers in any order).
+ * Outputs offsets[n+1]; targets/weights must hold 2*num_edges entries.
+ * Returns the arc count. */
+int64_t orc_assemble_unit(int64_t n, int64_t num_edges, const uint32_t *src, const uint32_t *dst,
+                          int64_t *offsets, int32_t *targets, float *weights) {
+    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(num_edges > 0 ? num_edges : 1));
+    uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(num_edges > 0 ? num_edges : 1));
+    for (int64_t e = 0; e < num_edges; ++e) {
+        uint64_t a = src[e], b = dst[e];
+        if (a > b) { uint64_t t = a; a = b; b = t; }
+        key[e] = (a << 32) | b;
+    }
+    int vb = ceil_log2((uint64_t)(n > 1 ? n : 2));
+    radix_sort_u64(key, tmp, num_edges, 32 + vb);
+    /* unique pairs + counts, in place */
+    int64_t np = 0;
+    double *cnt = (double *)tmp; /* reuse */
+    for (int64_t e = 0; e < num_edges; ++e) {
+        if (np > 0 && key[np - 1] == key[e]) cnt[np - 1] += 1.0;
+        else { key[np] = key[e]; cnt[np] = 1.0; ++np; }
+    }
+    int64_t *deg = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t p = 0; p < np; ++p) {
+        uint64_t a = key[p] >> 32, b = key[p] & 0xFFFFFFFFULL;
+        deg[a]++;
+        if (a != b) deg[b]++;
+    }
+    offsets[0] = 0;
+    for (int64_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + deg[i];
+    int64_t *cur = deg;
+    for (int64_t i = 0; i < n; ++i) cur[i] = offsets[i];
+    /* phase 1: arcs b->a with a<b land first in row b (targets < b, ascending a) */
+    for (int64_t p = 0; p < np; ++p) {
+        uint64_t a = key[p] >> 32, b = key[p] & 0xFFFFFFFFULL;
+        if (a != b) { int64_t s = cur[b]++; targets[s] = (int32_t)a; weights[s] = (float)cnt[p]; }
+    }
+    /* phase 2: arcs a->b with b>=a (ascending b) */
+    for (int64_t p = 0; p < np; ++p) {
+        uint64_t a = key[p] >> 32, b = key[p] & 0xFFFFFFFFULL;
+        int64_t s = cur[a]++;
+        targets[s] = (int32_t)b;
+        weights[s] = (float)cnt[p];
+    }
+    int64_t m = offsets[n];
+    free(deg); free(key); free(tmp);
+    return m;
+}

@@ -1,0 +1,95 @@
+"""Pin the CPU oracle against the reference's golden vectors (CPU only).
+
+Every golden case was produced by the Python reference (make_golden.py);
+the C restatement must reproduce labels after every sweep, delta_history,
+iterations, converged, lpa_move outputs and the metric tallies.
+"""
+
+import numpy as np
+import pytest
+
+from golden_io import Golden
+
+G = Golden()
+RUNS = G.names("run")
+MOVES = G.names("move")
+METRICS = G.names("metric")
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_oracle_run_matches_reference(oracle, name):
+    g = G.graph(name)
+    meta = G.meta(name)
+    cfg = G.cfg(name)
+    order = G.get(name, "order")
+    res = oracle.lpa_run(g, cfg, order=order, keep_history=meta["has_hist"])
+    assert res.iterations == meta["iterations"]
+    assert res.delta_history == meta["delta_history"]
+    assert res.converged == meta["converged"]
+    np.testing.assert_array_equal(res.labels, G.get(name, "labels"))
+    if meta["has_hist"]:
+        np.testing.assert_array_equal(res.label_history, G.get(name, "label_hist"))
+    assert oracle.aux_memory_estimate(g, cfg) == meta["aux_bytes"]
+
+
+@pytest.mark.parametrize("name", MOVES)
+def test_oracle_move_matches_reference(oracle, name):
+    g = G.graph(name)
+    meta = G.meta(name)
+    cfg = G.cfg(name)
+    labels = G.get(name, "in_labels").copy()
+    flags = G.get(name, "in_flags").copy()
+    delta = oracle.lpa_move(g, labels, flags, cfg, meta["pickless"], G.get(name, "order"))
+    assert delta == meta["delta"]
+    np.testing.assert_array_equal(labels, G.get(name, "out_labels"))
+    np.testing.assert_array_equal(flags, G.get(name, "out_flags"))
+
+
+@pytest.mark.parametrize("name", METRICS + [n for n in RUNS if G.meta(n)["modularity"] is not None][:60])
+def test_oracle_metrics_match_reference(oracle, name):
+    g = G.graph(name)
+    meta = G.meta(name)
+    labels = G.get(name, "labels")
+    sizes, internal, incident = oracle.tally(g, labels)
+    if meta["kind"] == "metric":
+        np.testing.assert_array_equal(sizes, G.get(name, "sizes"))
+        np.testing.assert_allclose(internal, G.get(name, "internal"), rtol=0, atol=1e-9)
+        np.testing.assert_allclose(incident, G.get(name, "incident"), rtol=0, atol=1e-9)
+    assert int(np.count_nonzero(sizes)) == meta["num_communities"]
+    assert oracle.modularity(g, labels) == pytest.approx(meta["modularity"], abs=1e-9)
+
+
+def test_generators_are_deterministic(oracle):
+    a = oracle.rmat(10, seed=3)
+    b = oracle.rmat(10, seed=3)
+    np.testing.assert_array_equal(a.offsets, b.offsets)
+    np.testing.assert_array_equal(a.targets, b.targets)
+    c = oracle.rmat(10, seed=4)
+    assert not np.array_equal(a.targets[:100], c.targets[:100]) or a.num_arcs != c.num_arcs
+
+
+def test_grid_shape(oracle):
+    g = oracle.grid(7, 9, permute=True)
+    assert g.num_vertices == 63
+    assert g.num_arcs == 2 * (7 * 8 + 6 * 9)
+    deg = np.diff(g.offsets)
+    assert deg.max() == 4 and deg.min() == 2
+
+
+def test_perm_is_bijection(oracle):
+    for n in (1, 2, 3, 17, 100, 1000):
+        vals = sorted(oracle.perm(x, n, 7) for x in range(n))
+        assert vals == list(range(n))
+
+
+def test_assemble_unit_matches_numpy_assemble(oracle):
+    from oracle.oracle import assemble
+    rng = np.random.default_rng(5)
+    n = 300
+    src = rng.integers(0, n, 3000).astype(np.uint32)
+    dst = rng.integers(0, n, 3000).astype(np.uint32)
+    g1 = oracle._assemble_unit(n, src, dst)
+    g2 = assemble(n, src, dst, np.ones(src.size))
+    np.testing.assert_array_equal(g1.offsets, g2.offsets)
+    np.testing.assert_array_equal(g1.targets, g2.targets)
+    np.testing.assert_array_equal(g1.weights, g2.weights)
