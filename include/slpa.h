@@ -1,0 +1,165 @@
+/*
+ * slpa.h -- C ABI of the B200-native label-propagation engine
+ *           (libslpa_b200.so, built from paper_2411_19901_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (sketchlpa 0.1.0, /root/reference/pkg/src/sketchlpa).  Each entry point
+ * names the reference interface it replaces.  Plain C types only: host
+ * pointers unless a name says `_device`.  Every call returns an slpa_status;
+ * slpa_last_error() gives the message.  A context owns one device, one
+ * stream, one resident graph and its work buffers; contexts are independent
+ * (no hidden globals), so one context per device / per thread.
+ */
+#ifndef SLPA_H
+#define SLPA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SLPA_OK = 0,
+    SLPA_EINVAL = 1,      /* bad argument / config  -> ValueError (lpa.py:62-80, :287-288; metrics.py:36-40, :71-72) */
+    SLPA_ECUDA = 2,       /* CUDA runtime failure   -> RuntimeError */
+    SLPA_EUNSUPPORTED = 3,/* option outside the GPU path's limits -> ValueError */
+    SLPA_ENOGRAPH = 4,    /* no graph resident */
+    SLPA_EHOOK = 5        /* iteration hook asked to abort (exception in the Python hook) */
+} slpa_status;
+
+enum { SLPA_VARIANT_EXACT = 0, SLPA_VARIANT_BM = 1, SLPA_VARIANT_MG = 2 };
+enum { SLPA_SCAN_SINGLE = 0, SLPA_SCAN_DOUBLE = 1 };
+
+/* Mirror of LpaConfig (lpa.py:44-60); validated like LpaConfig.validate()
+ * (lpa.py:62-80).  worker_count == 0 selects the deterministic mode whose
+ * results are bit-identical to the reference's sequential sweep
+ * (lpa.py:204-224); worker_count > 0 selects the asynchronous in-place GPU
+ * sweep (the analogue of the reference's threaded mode, lpa.py:242-259). */
+typedef struct {
+    int32_t variant;          /* SLPA_VARIANT_*                 lpa.py:51 */
+    int32_t scan_mode;        /* SLPA_SCAN_*                    lpa.py:52 */
+    int32_t sketch_slots;     /* k                              lpa.py:53 */
+    int32_t pickless_gap;     /* rho                            lpa.py:54 */
+    double  tolerance;        /* tau                            lpa.py:55 */
+    int32_t max_iterations;   /*                                lpa.py:56 */
+    int32_t degree_threshold; /* D_H                            lpa.py:57 */
+    int32_t partial_groups;   /* R_H                            lpa.py:58 */
+    int32_t worker_count;     /* 0 = deterministic, >0 = async  lpa.py:59 */
+    int32_t shared_sketch;    /*                                lpa.py:60 */
+} slpa_config;
+
+/* Called after every sweep, like iteration_hook(it, pickless, labels)
+ * (lpa.py:271-273, :297-298).  `labels` is a host copy indexed by vertex id.
+ * Return non-zero to abort the run (slpa_run then returns SLPA_EHOOK). */
+typedef int32_t (*slpa_hook_fn)(void *user, int32_t iteration, int32_t pickless, const int32_t *labels);
+
+typedef struct slpa_ctx slpa_ctx;
+
+/* Per-run counters (not part of the reference API; for measurement). */
+typedef struct {
+    int64_t sweeps;             /* iterations executed */
+    int64_t rounds;             /* speculative rounds (deterministic mode) */
+    int64_t vertex_evals;       /* vertex evaluations incl. re-evaluations */
+    int64_t arc_reads;          /* adjacency arcs scanned incl. re-evaluations */
+    int64_t first_evals;        /* evaluations in round 0 of each sweep (= processed vertices) */
+    int64_t first_arcs;         /* arcs scanned in round 0 (algorithmic arcs) */
+    double  device_ms;          /* device time of the last run (CUDA events) */
+    int64_t device_bytes;       /* bytes the context holds on the device */
+    int64_t graph_bytes;        /* of which the resident CSR */
+    int64_t kernel_launches;    /* kernels launched by the last run / move */
+} slpa_run_stats;
+
+/* Per-kernel-class device time when profiling is on (CUDA events on the
+ * context stream around every launch; adds a host sync per launch, so keep
+ * it off for throughput runs).  evals / arcs are the vertices evaluated and
+ * arcs scanned by those launches -- the algorithmic work. */
+enum {
+    SLPA_PROF_EVAL_LO0 = 0,  /* round-0 low-degree label scan (thread per vertex) */
+    SLPA_PROF_EVAL_HI0 = 1,  /* round-0 high-degree label scan (warp per vertex) */
+    SLPA_PROF_EVAL_LOK = 2,  /* re-evaluation rounds, low degree */
+    SLPA_PROF_EVAL_HIK = 3,  /* re-evaluation rounds, high degree */
+    SLPA_PROF_COMPACT = 4,   /* dirty bitmap -> worklists */
+    SLPA_PROF_COMMIT = 5,    /* label update, flags, changed-vertex count */
+    SLPA_PROF_OTHER = 6,
+    SLPA_PROF_N = 8
+};
+typedef struct {
+    int64_t launches[SLPA_PROF_N];
+    double ms[SLPA_PROF_N];
+    int64_t evals[SLPA_PROF_N];
+    int64_t arcs[SLPA_PROF_N];
+} slpa_profile;
+
+/* ---------------------------------------------------------------- context */
+int32_t slpa_create(int32_t device, slpa_ctx **out);
+int32_t slpa_destroy(slpa_ctx *ctx);
+const char *slpa_last_error(const slpa_ctx *ctx);   /* ctx may be NULL (creation errors) */
+const char *slpa_version(void);
+/* The CUDA stream all work is issued on (cudaStream_t as an integer). */
+int32_t slpa_stream(slpa_ctx *ctx, uint64_t *stream_out);
+
+/* ------------------------------------------------------------ graph upload
+ * Replaces handing a sketchlpa Graph (graph.py:35-74: offsets int64[n+1],
+ * targets int32[m], weights float32|float64[m]) to lpa_run/lpa_move.  The
+ * library copies the arrays (the caller's Graph stays immutable,
+ * graph.py:73-74), checks the Graph invariants (graph.py:55-68), detects
+ * whether the arc set is symmetric, and, when `order` is given (lpa.py:283-
+ * 288, a permutation of 0..n-1), stores vertices in visiting order while
+ * label values stay original ids. */
+int32_t slpa_graph_upload(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *offsets,
+                          const int32_t *targets, const void *weights, int32_t weights_f64,
+                          const int64_t *order);
+/* Same, from device pointers (e.g. torch CUDA tensors' data_ptr()). */
+int32_t slpa_graph_upload_device(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *offsets,
+                                 const int32_t *targets, const void *weights, int32_t weights_f64,
+                                 const int64_t *order);
+/* Re-order the resident graph for a new `order` (NULL = ascending ids). */
+int32_t slpa_graph_set_order(slpa_ctx *ctx, const int64_t *order);
+int32_t slpa_graph_info(slpa_ctx *ctx, int64_t *n, int64_t *m, int32_t *weights_f64, int32_t *symmetric);
+/* Copy the resident CSR (in original id order) back to host buffers. */
+int32_t slpa_graph_download(slpa_ctx *ctx, int64_t *offsets, int32_t *targets, void *weights);
+
+/* ----------------------------------------------------- synthetic graphs
+ * Device-side generators + canonical assembly (graph.py:107-139 rules:
+ * unordered pairs, duplicates summed, self-loop kept once, sorted rows).
+ * Specified in DESIGN.md §6 and reproduced bit-for-bit by oracle/lpa_oracle.c.
+ * The graph becomes resident in the context. */
+int32_t slpa_gen_rmat(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
+                      uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key);
+int32_t slpa_gen_grid(slpa_ctx *ctx, int64_t rows, int64_t cols, int32_t permute, uint64_t perm_key);
+int32_t slpa_gen_kmer(slpa_ctx *ctx, int64_t n, uint32_t keep, uint64_t seed, int32_t permute,
+                      uint64_t perm_key);
+/* build_graph (graph.py:142-162) from a host edge list; w may be NULL (1.0). */
+int32_t slpa_build_graph(slpa_ctx *ctx, int64_t n, int64_t num_edges, const int64_t *src,
+                         const int64_t *dst, const double *w, int32_t weights_f64);
+
+/* ------------------------------------------------------------ label propagation
+ * lpa_run (lpa.py:262-308).  labels_out: host int32[n] or NULL (labels stay
+ * resident, fetch with slpa_get_labels).  delta_history: host int64[max_iterations]. */
+int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int64_t *delta_history,
+                 int32_t *iterations, int32_t *converged, slpa_hook_fn hook, void *hook_user);
+/* lpa_move (lpa.py:227-259): one sweep on caller state.  labels int32[n] and
+ * unprocessed uint8[n] (numpy bool) are read and written back in place. */
+int32_t slpa_move(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels, uint8_t *unprocessed,
+                  int32_t pickless, int64_t *changed);
+/* Final labels of the last run, by vertex id. */
+int32_t slpa_get_labels(slpa_ctx *ctx, int32_t *labels_out);
+int32_t slpa_last_run_stats(slpa_ctx *ctx, slpa_run_stats *out);
+/* Profiling switch (resets the accumulated profile) and read-out. */
+int32_t slpa_set_profiling(slpa_ctx *ctx, int32_t on);
+int32_t slpa_get_profile(slpa_ctx *ctx, slpa_profile *out);
+/* aux_memory_estimate (lpa.py:311-333) -- the reference's formula. */
+int64_t slpa_aux_memory_estimate(int64_t n, int32_t value_bytes, const slpa_config *cfg);
+
+/* ------------------------------------------------------------ metrics
+ * _tally / community_stats / modularity (metrics.py:34-74).  labels: host
+ * int32[n] by vertex id, or NULL for the resident labels of the last run.
+ * sizes/internal/incident may be NULL. */
+int32_t slpa_modularity(slpa_ctx *ctx, const int32_t *labels, double *q, int64_t *num_communities,
+                        int64_t *sizes, double *internal, double *incident);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLPA_H */

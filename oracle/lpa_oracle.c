@@ -163,17 +163,23 @@ static void scratch_free(scratch_t *sc) {
     free(sc->idx); free(sc->lab); free(sc->wt);
 }
 
-static int32_t select_mg(const orc_graph *g, const int32_t *labels, int64_t i,
+/* Label of neighbour j as seen by vertex i: the sequential sweep reads
+ * in place, so lab_lo == lab_hi == labels.  The sweep verifier passes the
+ * end-of-sweep labels (lower positions) and start-of-sweep labels (higher
+ * positions) instead. */
+#define LAB(j) ((j) < i ? lab_lo[(j)] : lab_hi[(j)])
+
+static int32_t select_mg(const orc_graph *g, const int32_t *lab_lo, const int32_t *lab_hi, int64_t i,
                          const orc_config *cfg, scratch_t *sc) { /* lpa.py:153-193 */
     int64_t lo = g->offsets[i], hi = g->offsets[i + 1], deg = hi - lo;
-    int32_t cur = labels[i];
+    int32_t cur = lab_hi[i];
     if (deg == 0) return cur;
     mg_t *sk = &sc->parts[0];
     if (deg < cfg->degree_threshold || cfg->shared_sketch) {
         mg_reset(sk);
         for (int64_t a = lo; a < hi; ++a) {
             int32_t j = g->targets[a];
-            if (j != i) mg_accumulate(sk, labels[j], arc_w(g, a));
+            if (j != i) mg_accumulate(sk, LAB(j), arc_w(g, a));
         }
     } else {
         int P = cfg->partial_groups;
@@ -184,7 +190,7 @@ static int32_t select_mg(const orc_graph *g, const int32_t *labels, int64_t i,
             chunk_bounds(deg, P, p, &s, &e);
             for (int64_t t = s; t < e; ++t) {
                 int32_t j = g->targets[lo + t];
-                if (j != i) mg_accumulate(part, labels[j], arc_w(g, lo + t));
+                if (j != i) mg_accumulate(part, LAB(j), arc_w(g, lo + t));
             }
         }
         for (int p = 1; p < P; ++p) mg_merge(sk, &sc->parts[p]);
@@ -193,23 +199,23 @@ static int32_t select_mg(const orc_graph *g, const int32_t *labels, int64_t i,
         for (int s = 0; s < sk->k; ++s) sk->vals[s] = 0.0; /* clear_values sketch.py:107-111 */
         for (int64_t a = lo; a < hi; ++a) {
             int32_t j = g->targets[a];
-            if (j != i) mg_rescan_add(sk, labels[j], arc_w(g, a));
+            if (j != i) mg_rescan_add(sk, LAB(j), arc_w(g, a));
         }
     }
     int32_t best;
     return mg_max_key(sk, &best) ? best : cur;
 }
 
-static int32_t select_bm(const orc_graph *g, const int32_t *labels, int64_t i,
+static int32_t select_bm(const orc_graph *g, const int32_t *lab_lo, const int32_t *lab_hi, int64_t i,
                          const orc_config *cfg) { /* lpa.py:121-150 */
     int64_t lo = g->offsets[i], hi = g->offsets[i + 1], deg = hi - lo;
-    int32_t cur = labels[i];
+    int32_t cur = lab_hi[i];
     if (deg == 0) return cur;
     if (deg < cfg->degree_threshold) {
         bm_t st = {cur, 0.0};
         for (int64_t a = lo; a < hi; ++a) {
             int32_t j = g->targets[a];
-            if (j != i) bm_accumulate(&st, labels[j], arc_w(g, a));
+            if (j != i) bm_accumulate(&st, LAB(j), arc_w(g, a));
         }
         return st.cand;
     }
@@ -221,7 +227,7 @@ static int32_t select_bm(const orc_graph *g, const int32_t *labels, int64_t i,
         chunk_bounds(deg, P, p, &s, &e);
         for (int64_t t = s; t < e; ++t) {
             int32_t j = g->targets[lo + t];
-            if (j != i) bm_accumulate(&st, labels[j], arc_w(g, lo + t));
+            if (j != i) bm_accumulate(&st, LAB(j), arc_w(g, lo + t));
         }
         /* reduce_votes sketch.py:165-181 */
         if (p == 0 || st.w > best.w || (st.w == best.w && st.cand < best.cand)) best = st;
@@ -237,7 +243,7 @@ static int cmp_lab_pos(const void *pa, const void *pb) {
     return a < b ? -1 : (a > b ? 1 : 0);
 }
 
-static int32_t select_exact(const orc_graph *g, const int32_t *labels, int64_t i,
+static int32_t select_exact(const orc_graph *g, const int32_t *lab_lo, const int32_t *lab_hi, int64_t i,
                             scratch_t *sc) { /* lpa.py:92-107 */
     int64_t lo = g->offsets[i], hi = g->offsets[i + 1], deg = hi - lo;
     if (deg > sc->cap) {
@@ -250,12 +256,12 @@ static int32_t select_exact(const orc_graph *g, const int32_t *labels, int64_t i
     for (int64_t a = lo; a < hi; ++a) {
         int32_t j = g->targets[a];
         if (j == i) continue;
-        sc->lab[cnt] = labels[j];
+        sc->lab[cnt] = LAB(j);
         sc->wt[cnt] = arc_w(g, a);
         sc->idx[cnt] = cnt;
         ++cnt;
     }
-    if (cnt == 0) return labels[i];
+    if (cnt == 0) return lab_hi[i];
     /* np.bincount adds weights in input order per label: stable sort by
      * (label, position) then left-to-right sums reproduce that order. */
     g_sort_lab = sc->lab;
@@ -272,11 +278,16 @@ static int32_t select_exact(const orc_graph *g, const int32_t *labels, int64_t i
     return best;
 }
 
+static int32_t select_view(const orc_graph *g, const int32_t *lab_lo, const int32_t *lab_hi, int64_t i,
+                           const orc_config *cfg, scratch_t *sc) { /* lpa.py:196-201 */
+    if (cfg->variant == ORC_EXACT) return select_exact(g, lab_lo, lab_hi, i, sc);
+    if (cfg->variant == ORC_BM) return select_bm(g, lab_lo, lab_hi, i, cfg);
+    return select_mg(g, lab_lo, lab_hi, i, cfg, sc);
+}
+
 static int32_t select_any(const orc_graph *g, const int32_t *labels, int64_t i,
-                          const orc_config *cfg, scratch_t *sc) { /* lpa.py:196-201 */
-    if (cfg->variant == ORC_EXACT) return select_exact(g, labels, i, sc);
-    if (cfg->variant == ORC_BM) return select_bm(g, labels, i, cfg);
-    return select_mg(g, labels, i, cfg, sc);
+                          const orc_config *cfg, scratch_t *sc) {
+    return select_view(g, labels, labels, i, cfg, sc);
 }
 
 /* ------------------------------------------------------------ public API */
@@ -571,4 +582,47 @@ int64_t orc_assemble_unit(int64_t n, int64_t num_edges, const uint32_t *src, con
     int64_t m = offsets[n];
     free(deg); free(key); free(tmp);
     return m;
+}
+
+/* ==================================================================== */
+/*  Sweep verifier (test tool).  For an ascending-order sweep, vertex v's  */
+/*  turn and output are a function of L1 (end labels) of lower vertices,  */
+/*  L0 (start labels) of higher ones and F0[v]; that system has a unique */
+/*  solution, the sequential sweep.  Checking it vertex by vertex proves  */
+/*  (for all vertices) or samples (for a subset) bit-exactness at any     */
+/*  scale.  Also checks F1 (end flags).  Symmetric graphs only.           */
+/*  Returns the number of sampled vertices that disagree; the first bad  */
+/*  vertex is written to *first_bad (or -1).                              */
+/* ==================================================================== */
+int64_t orc_verify_sweep(const orc_graph *g, const int32_t *L0, const uint8_t *F0, const int32_t *L1,
+                         const uint8_t *F1, const orc_config *cfg, int32_t pickless,
+                         const int64_t *vertices, int64_t count, int64_t *first_bad) {
+    scratch_t sc;
+    scratch_init(&sc, cfg);
+    int64_t bad = 0;
+    *first_bad = -1;
+    for (int64_t q = 0; q < count; ++q) {
+        int64_t v = vertices ? vertices[q] : q;
+        int64_t lo = g->offsets[v], hi = g->offsets[v + 1];
+        int turn = F0[v] != 0, f1 = 0;
+        for (int64_t a = lo; a < hi; ++a) {
+            int32_t u = g->targets[a];
+            int chg_u = L1[u] != L0[u];
+            if (u < v && chg_u) turn = 1;
+            if (u > v && chg_u) f1 = 1;
+            if (u == v && chg_u) f1 = 1; /* self-loop re-marks itself */
+        }
+        int32_t expect = L0[v];
+        if (turn) {
+            int32_t cand = select_view(g, L1, L0, v, cfg, &sc);
+            if (cand != L0[v] && (!pickless || cand < L0[v])) expect = cand;
+        }
+        int ok = (L1[v] == expect) && ((F1[v] != 0) == f1);
+        if (!ok) {
+            if (*first_bad < 0) *first_bad = v;
+            ++bad;
+        }
+    }
+    scratch_free(&sc);
+    return bad;
 }

@@ -191,6 +191,8 @@ class Oracle:
         L.orc_tally.argtypes = [vp, vp, vp, vp, vp]
         L.orc_aux_memory_estimate.restype = i64
         L.orc_aux_memory_estimate.argtypes = [i64, i32, vp, i32]
+        L.orc_verify_sweep.restype = i64
+        L.orc_verify_sweep.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, i64, vp]
         L.orc_perm.restype = u64
         L.orc_perm.argtypes = [u64, u64, u64]
         L.orc_rmat_edges.restype = i64
@@ -258,6 +260,22 @@ class Oracle:
         it = iters.value
         return OracleResult(labels, it, [int(x) for x in delta[:it]], bool(conv.value),
                             None if hist is None else hist[:it].copy())
+
+    def verify_sweep(self, g, L0, F0, L1, F1, cfg, pickless, vertices=None):
+        """Check a GPU sweep (L0,F0) -> (L1,F1) vertex by vertex (ascending
+        order, symmetric graph).  Returns (mismatches, first_bad_vertex)."""
+        gs, keep = self._graph(g)
+        c = _cfg_struct(cfg)
+        arrs = [np.ascontiguousarray(L0, dtype=np.int32), np.ascontiguousarray(F0).view(np.uint8),
+                np.ascontiguousarray(L1, dtype=np.int32), np.ascontiguousarray(F1).view(np.uint8)]
+        vs = None if vertices is None else np.ascontiguousarray(vertices, dtype=np.int64)
+        count = int(g.num_vertices) if vs is None else int(vs.size)
+        first = ctypes.c_int64(-1)
+        bad = self.lib.orc_verify_sweep(ctypes.byref(gs), arrs[0].ctypes.data, arrs[1].ctypes.data,
+                                        arrs[2].ctypes.data, arrs[3].ctypes.data, ctypes.byref(c),
+                                        1 if pickless else 0, None if vs is None else vs.ctypes.data,
+                                        count, ctypes.byref(first))
+        return int(bad), int(first.value)
 
     def tally(self, g, labels):
         n = int(g.num_vertices)

@@ -1,0 +1,748 @@
+// slpa_graph.cu -- resident CSR management: validation (graph.py:55-68),
+// symmetry detection + reverse CSR, visiting-order permutation (lpa.py:283-288),
+// degree binning (lpa.py:137, :173), and device-side synthetic generators with
+// canonical assembly (graph.py:107-139).  One-time setup work; the sweep
+// kernels are in slpa_sweep.cu.
+#include <cmath>
+#include <vector>
+#include <cub/cub.cuh>
+#include "slpa_internal.cuh"
+
+namespace {
+constexpr int kT = 256;
+
+// ------------------------------------------------------------------ validation
+// err bits: 1 offsets[0] != 0, 2 decreasing offsets, 4 offsets[n] != m,
+//           8 target out of range, 16 weight not > 0
+__global__ void k_validate_offsets(const int64_t *off, int64_t n, int64_t m, unsigned *err) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == 0 && off[0] != 0) atomicOr(err, 1u);
+    if (i < n && off[i + 1] < off[i]) atomicOr(err, 2u);
+    if (i == n && off[n] != m) atomicOr(err, 4u);
+}
+template <class W>
+__global__ void k_validate_arcs(const int32_t *tgt, const W *w, int64_t n, int64_t m, unsigned *err) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    int32_t t = tgt[i];
+    if (t < 0 || t >= n) atomicOr(err, 8u);
+    if (!(w[i] > (W)0)) atomicOr(err, 16u);
+}
+
+// ------------------------------------------------------------------ symmetry
+// Symmetric (for dependency purposes) iff every row is sorted and every arc
+// u->t has a reverse arc t->u.  One warp per vertex.
+__global__ void k_check_symmetric(const int64_t *off, const int32_t *tgt, int64_t n, unsigned *asym) {
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+        const int64_t lo = off[v], hi = off[v + 1];
+        bool bad = false;
+        for (int64_t e = lo + lane; e < hi; e += 32) {
+            int32_t t = tgt[e];
+            if (e > lo && tgt[e - 1] > t) bad = true;
+            // binary search v in row t
+            int64_t a = off[t], b = off[t + 1];
+            while (a < b) {
+                int64_t mid = (a + b) >> 1;
+                if (tgt[mid] < v) a = mid + 1;
+                else b = mid;
+            }
+            if (a >= off[t + 1] || tgt[a] != v) bad = true;
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(asym, 1u);
+    }
+}
+
+__global__ void k_in_degree(const int64_t *off, const int32_t *tgt, int64_t n, int64_t *indeg) {
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps)
+        for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32)
+            atomicAdd((unsigned long long *)&indeg[tgt[e]], 1ull);
+}
+__global__ void k_fill_reverse(const int64_t *off, const int32_t *tgt, int64_t n, int64_t *cursor, int32_t *rsrc) {
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps)
+        for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+            unsigned long long p = atomicAdd((unsigned long long *)&cursor[tgt[e]], 1ull);
+            rsrc[p] = (int32_t)v;
+        }
+}
+
+// ------------------------------------------------------------------ order
+__global__ void k_order_scatter(const int64_t *order, int64_t n, int32_t *ids, int32_t *pos, unsigned *seen,
+                                unsigned *err) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int64_t id = order[p];
+    if (id < 0 || id >= n) {
+        atomicOr(err, 1u);
+        return;
+    }
+    ids[p] = (int32_t)id;
+    pos[id] = (int32_t)p;
+    if (atomicAdd(&seen[id], 1u) != 0) atomicOr(err, 1u);
+}
+__global__ void k_perm_degree(const int64_t *off, const int32_t *ids, int64_t n, int64_t *deg) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int32_t id = ids[p];
+    deg[p] = off[id + 1] - off[id];
+}
+template <class W>
+__global__ void k_perm_rows(const int64_t *off, const int32_t *tgt, const W *w, const int32_t *ids, const int32_t *pos,
+                            const int64_t *poff, int32_t *ptgt, W *pw, int64_t n) {
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += warps) {
+        const int32_t id = ids[p];
+        const int64_t lo = off[id], hi = off[id + 1], dst = poff[p];
+        for (int64_t e = lo + lane; e < hi; e += 32) {
+            ptgt[dst + (e - lo)] = pos[tgt[e]];
+            pw[dst + (e - lo)] = w[e];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ bins
+__global__ void k_classify(const int64_t *off, int64_t n, int32_t thr, int32_t single, uint8_t *cls) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int64_t d = off[v + 1] - off[v];
+    cls[v] = d == 0 ? CLS_NONE : ((single || d < thr) ? CLS_LO : CLS_HI);
+}
+struct IsClass {
+    const uint8_t *cls;
+    uint8_t c;
+    __host__ __device__ bool operator()(const int32_t &v) const { return cls[v] == c; }
+};
+__global__ void k_bin_degrees(const int64_t *off, const int32_t *bin, int64_t cnt, int64_t *deg) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) deg[i] = off[bin[i] + 1] - off[bin[i]];
+}
+
+// ------------------------------------------------------------------ generators
+// Specification: DESIGN.md §6; CPU twin: oracle/lpa_oracle.c.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t h64(uint64_t seed, uint64_t ctr) { return splitmix64(splitmix64(seed) ^ ctr); }
+__device__ __forceinline__ uint64_t perm_pow2(uint64_t x, int b, uint64_t key) {
+    if (b == 0) return 0;
+    uint64_t mask = (b >= 64) ? ~0ULL : ((1ULL << b) - 1);
+    int sh = b / 2 + 1;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        uint64_t k = splitmix64(key + (uint64_t)r);
+        x = (x * (k | 1ULL)) & mask;
+        if (sh < b) x ^= x >> sh;
+        x = (x + (k >> 17)) & mask;
+    }
+    return x;
+}
+__device__ __forceinline__ uint64_t perm_n(uint64_t x, uint64_t n, int b, uint64_t key) {
+    uint64_t y = perm_pow2(x, b, key);
+    while (y >= n) y = perm_pow2(y, b, key);
+    return y;
+}
+
+// Edge keys: (min << 32 | max); dropped edges (self-loops) get `drop`.
+__global__ void k_gen_rmat(int32_t scale, int64_t e0, int64_t count, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                           uint64_t seed, int32_t permute, uint64_t perm_key, uint64_t drop, uint64_t *keys) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t e = e0 + i;
+    const uint64_t W = (uint64_t)(scale + 1) / 2;
+    uint64_t u = 0, v = 0, word = 0;
+    for (int l = 0; l < scale; ++l) {
+        if ((l & 1) == 0) word = h64(seed, (uint64_t)e * W + (uint64_t)(l >> 1));
+        uint32_t r = (l & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+        uint64_t bit = 1ULL << (scale - 1 - l);
+        if (r < tA) {
+        } else if (r < tAB) v |= bit;
+        else if (r < tABC) u |= bit;
+        else { u |= bit; v |= bit; }
+    }
+    if (permute) {
+        u = perm_pow2(u, scale, perm_key);
+        v = perm_pow2(v, scale, perm_key);
+    }
+    if (u == v) { keys[i] = drop; return; }
+    uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    keys[i] = (a << 32) | b;
+}
+
+__global__ void k_gen_grid(int64_t rows, int64_t cols, int32_t permute, uint64_t perm_key, int bits, uint64_t drop,
+                           uint64_t *keys) {
+    // edge index: 2 per cell (right, down)
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = rows * cols;
+    if (i >= 2 * n) return;
+    const int64_t cell = i >> 1;
+    const int64_t r = cell / cols, c = cell % cols;
+    uint64_t v = (uint64_t)cell, w;
+    if ((i & 1) == 0) {
+        if (c + 1 >= cols) { keys[i] = drop; return; }
+        w = v + 1;
+    } else {
+        if (r + 1 >= rows) { keys[i] = drop; return; }
+        w = v + (uint64_t)cols;
+    }
+    if (permute) {
+        v = perm_n(v, (uint64_t)n, bits, perm_key);
+        w = perm_n(w, (uint64_t)n, bits, perm_key);
+    }
+    uint64_t a = v < w ? v : w, b = v < w ? w : v;
+    keys[i] = (a << 32) | b;
+}
+
+__global__ void k_gen_kmer(int64_t n, uint32_t keep, uint64_t seed, int32_t permute, uint64_t perm_key, int bits,
+                           uint64_t drop, uint64_t *keys) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t chords = n / 20;
+    if (i >= (n - 1) + chords) return;
+    uint64_t a, b;
+    if (i < n - 1) {
+        uint64_t x = h64(seed, (uint64_t)i);
+        if ((uint32_t)(x >> 32) >= keep) { keys[i] = drop; return; }
+        a = (uint64_t)i;
+        b = (uint64_t)i + 1;
+    } else {
+        int64_t c = i - (n - 1);
+        uint64_t x = h64(seed ^ 0xC0DEULL, (uint64_t)c);
+        a = (uint64_t)(uint32_t)x % (uint64_t)n;
+        b = (x >> 32) % (uint64_t)n;
+        if (a == b) { keys[i] = drop; return; }
+    }
+    if (permute) {
+        a = perm_n(a, (uint64_t)n, bits, perm_key);
+        b = perm_n(b, (uint64_t)n, bits, perm_key);
+    }
+    uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+    keys[i] = (lo << 32) | hi;
+}
+
+// unique pairs (a<=b, count) -> arc keys (src<<32|dst) with weights
+__global__ void k_pair_arity(const uint64_t *pairs, int64_t np, int64_t *arity) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    uint64_t p = pairs[i];
+    arity[i] = ((p >> 32) == (p & 0xFFFFFFFFULL)) ? 1 : 2;
+}
+template <class W>
+__global__ void k_emit_arcs(const uint64_t *pairs, const double *wsum, const int64_t *pos, int64_t np, uint64_t *akeys,
+                            W *aw) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    uint64_t p = pairs[i];
+    uint64_t a = p >> 32, b = p & 0xFFFFFFFFULL;
+    int64_t o = pos[i];
+    akeys[o] = (a << 32) | b;
+    aw[o] = (W)wsum[i];
+    if (a != b) {
+        akeys[o + 1] = (b << 32) | a;
+        aw[o + 1] = (W)wsum[i];
+    }
+}
+__global__ void k_counts_to_double(const uint32_t *cnt, int64_t np, double *w) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < np) w[i] = (double)cnt[i];
+}
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src),
+// which np.add.reduceat applies to every segment after its first element.
+__device__ __noinline__ double np_pairwise(const double *v, const int64_t *idx, int64_t n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int64_t i = 0; i < n; ++i) res += v[idx[i]];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = v[idx[j]];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += v[idx[i + j]];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += v[idx[i]];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(v, idx, n2) + np_pairwise(v, idx + n2, n - n2);
+}
+// graph.py:127: pw = np.add.reduceat(w, starts) over the stably sorted entries
+__global__ void k_run_sums(const double *w, const int64_t *idx, const int64_t *start, const uint32_t *cnt, int64_t np,
+                           double *out) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= np) return;
+    const int64_t s = start[r], c = cnt[r];
+    double acc = w[idx[s]];
+    if (c > 1) acc += np_pairwise(w, idx + s + 1, c - 1);
+    out[r] = acc;
+}
+__global__ void k_pair_keys(const int64_t *src, const int64_t *dst, int64_t ne, uint64_t *keys, int64_t *idx) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ne) return;
+    uint64_t a = (uint64_t)src[i], b = (uint64_t)dst[i];
+    keys[i] = a < b ? ((a << 32) | b) : ((b << 32) | a);
+    idx[i] = i;
+}
+// offsets[v] = lower_bound(akeys, v << 32)
+__global__ void k_offsets_from_keys(const uint64_t *akeys, int64_t m, int64_t n, int64_t *off) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v > n) return;
+    uint64_t key = (uint64_t)v << 32;
+    int64_t a = 0, b = m;
+    while (a < b) {
+        int64_t mid = (a + b) >> 1;
+        if (akeys[mid] < key) a = mid + 1;
+        else b = mid;
+    }
+    off[v] = a;
+}
+__global__ void k_low32(const uint64_t *akeys, int64_t m, int32_t *tgt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) tgt[i] = (int32_t)(akeys[i] & 0xFFFFFFFFULL);
+}
+
+int ceil_log2(uint64_t n) {
+    int b = 0;
+    while ((1ULL << b) < n) ++b;
+    return b;
+}
+
+unsigned read_flag(slpa_ctx *ctx, unsigned *d) {
+    unsigned h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return h;
+}
+
+template <class F>
+void cub_call(slpa_ctx *ctx, F &&f) {
+    size_t need = 0;
+    CUDA_TRY(f((void *)nullptr, need));
+    ctx->wb.scratch.alloc(need + 1);
+    CUDA_TRY(f((void *)ctx->wb.scratch.p, need));
+}
+
+unsigned grid_warps(int64_t items) {
+    int64_t b = (items * 32 + kT - 1) / kT;
+    if (b > 148 * 64) b = 148 * 64;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+}  // namespace
+
+// =====================================================================
+void slpa_graph_validate(slpa_ctx *ctx, const Csr &c, int w_f64) {
+    DevBuf<unsigned> err;
+    err.alloc(1);
+    CUDA_TRY(cudaMemsetAsync(err.p, 0, sizeof(unsigned), ctx->stream));
+    k_validate_offsets<<<grid_for(c.n + 1, kT), kT, 0, ctx->stream>>>(c.off.p, c.n, c.m, err.p);
+    if (c.m > 0) {
+        if (w_f64)
+            k_validate_arcs<double><<<grid_for(c.m, kT), kT, 0, ctx->stream>>>(c.tgt.p, c.w64.p, c.n, c.m, err.p);
+        else
+            k_validate_arcs<float><<<grid_for(c.m, kT), kT, 0, ctx->stream>>>(c.tgt.p, c.w32.p, c.n, c.m, err.p);
+    }
+    CUDA_TRY(cudaGetLastError());
+    unsigned e = read_flag(ctx, err.p);
+    err.release();
+    if (e & 1) throw SlpaError{SLPA_EINVAL, "offsets must be a 1-d array starting at 0"};
+    if (e & 2) throw SlpaError{SLPA_EINVAL, "offsets must be non-decreasing"};
+    if (e & 4) throw SlpaError{SLPA_EINVAL, "offsets[-1] must equal the arc count"};
+    if (e & 8) throw SlpaError{SLPA_EINVAL, "arc target out of range"};
+    if (e & 16) throw SlpaError{SLPA_EINVAL, "arc weights must be positive"};
+}
+
+// Symmetry check + reverse CSR of the active numbering; resets the bins.
+void slpa_graph_finalize(slpa_ctx *ctx) {
+    DeviceGraph &g = ctx->g;
+    cudaStream_t s = ctx->stream;
+    g.bin_thr = -1;
+    g.bin_single = -1;
+    g.roff.release();
+    g.rsrc.release();
+    g.symmetric = 1;
+    if (g.n == 0 || g.m == 0) return;
+    DevBuf<unsigned> flag;
+    flag.alloc(1);
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), s));
+    k_check_symmetric<<<grid_warps(g.n), kT, 0, s>>>(g.off(), g.tgt(), g.n, flag.p);
+    CUDA_TRY(cudaGetLastError());
+    g.symmetric = read_flag(ctx, flag.p) == 0;
+    flag.release();
+    if (g.symmetric) return;
+    // reverse CSR: in-degree histogram, exclusive scan, atomic fill
+    g.roff.alloc(g.n + 1);
+    g.rsrc.alloc(g.m);
+    DevBuf<int64_t> cursor;
+    cursor.alloc(g.n + 1);
+    CUDA_TRY(cudaMemsetAsync(cursor.p, 0, (g.n + 1) * sizeof(int64_t), s));
+    k_in_degree<<<grid_warps(g.n), kT, 0, s>>>(g.off(), g.tgt(), g.n, cursor.p);
+    int64_t *in = cursor.p, *out = g.roff.p;
+    int64_t nn = g.n + 1;
+    cub_call(ctx, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, nn, s);
+    });
+    CUDA_TRY(cudaMemcpyAsync(cursor.p, g.roff.p, (g.n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    k_fill_reverse<<<grid_warps(g.n), kT, 0, s>>>(g.off(), g.tgt(), g.n, cursor.p, g.rsrc.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cursor.release();
+}
+
+// Visiting order (lpa.py:283-288): order[p] = vertex visited p-th.
+void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order, bool on_device) {
+    DeviceGraph &g = ctx->g;
+    cudaStream_t s = ctx->stream;
+    g.perm.release();
+    g.ids.release();
+    g.pos.release();
+    g.has_order = 0;
+    if (!order) {
+        slpa_graph_finalize(ctx);
+        return;
+    }
+    const int64_t n = g.n, m = g.m;
+    DevBuf<int64_t> d_order;
+    const int64_t *ord = order;
+    if (!on_device) {
+        d_order.alloc(n);
+        CUDA_TRY(cudaMemcpyAsync(d_order.p, order, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        ord = d_order.p;
+    }
+    g.ids.alloc(n);
+    g.pos.alloc(n);
+    DevBuf<unsigned> seen, err;
+    seen.alloc(n);
+    err.alloc(1);
+    CUDA_TRY(cudaMemsetAsync(seen.p, 0, n * sizeof(unsigned), s));
+    CUDA_TRY(cudaMemsetAsync(err.p, 0, sizeof(unsigned), s));
+    if (n > 0) k_order_scatter<<<grid_for(n, kT), kT, 0, s>>>(ord, n, g.ids.p, g.pos.p, seen.p, err.p);
+    CUDA_TRY(cudaGetLastError());
+    if (read_flag(ctx, err.p)) {
+        g.ids.release();
+        g.pos.release();
+        throw SlpaError{SLPA_EINVAL, "order must be a permutation of all vertex ids"};
+    }
+    seen.release();
+    err.release();
+    d_order.release();
+    // permuted CSR
+    g.perm.n = n;
+    g.perm.m = m;
+    g.perm.off.alloc(n + 1);
+    g.perm.tgt.alloc(m);
+    if (g.w_f64) g.perm.w64.alloc(m);
+    else g.perm.w32.alloc(m);
+    DevBuf<int64_t> deg;
+    deg.alloc(n + 1);
+    CUDA_TRY(cudaMemsetAsync(deg.p, 0, (n + 1) * sizeof(int64_t), s));
+    if (n > 0) k_perm_degree<<<grid_for(n, kT), kT, 0, s>>>(g.base.off.p, g.ids.p, n, deg.p);
+    int64_t *din = deg.p, *dout = g.perm.off.p;
+    int64_t nn = n + 1;
+    cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceScan::ExclusiveSum(tmp, bytes, din, dout, nn, s); });
+    if (n > 0) {
+        if (g.w_f64)
+            k_perm_rows<double><<<grid_warps(n), kT, 0, s>>>(g.base.off.p, g.base.tgt.p, g.base.w64.p, g.ids.p, g.pos.p,
+                                                             g.perm.off.p, g.perm.tgt.p, g.perm.w64.p, n);
+        else
+            k_perm_rows<float><<<grid_warps(n), kT, 0, s>>>(g.base.off.p, g.base.tgt.p, g.base.w32.p, g.ids.p, g.pos.p,
+                                                            g.perm.off.p, g.perm.tgt.p, g.perm.w32.p, n);
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    deg.release();
+    g.has_order = 1;
+    slpa_graph_finalize(ctx);
+}
+
+// Degree bins for a threshold (lpa.py:137, :173): low = 0 < deg < thr
+// (ascending position), high = deg >= thr (descending degree, so the longest
+// scans start first).  `single` puts every non-empty vertex in the low bin.
+void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
+    DeviceGraph &g = ctx->g;
+    cudaStream_t s = ctx->stream;
+    const int single = (cfg->variant == SLPA_VARIANT_EXACT) || (cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch);
+    if (g.bin_thr == cfg->degree_threshold && g.bin_single == single) return;
+    const int64_t n = g.n;
+    g.cls.alloc(n);
+    g.bin_lo.alloc(n);
+    g.bin_hi.alloc(n);
+    if (n > 0) k_classify<<<grid_for(n, kT), kT, 0, s>>>(g.off(), n, cfg->degree_threshold, single, g.cls.p);
+    CUDA_TRY(cudaGetLastError());
+    DevBuf<int64_t> cnt;
+    cnt.alloc(2);
+    cub::CountingInputIterator<int32_t> it(0);
+    for (int which = 0; which < 2; ++which) {
+        IsClass pred{g.cls.p, (uint8_t)(which == 0 ? CLS_LO : CLS_HI)};
+        int32_t *out = which == 0 ? g.bin_lo.p : g.bin_hi.p;
+        int64_t *nsel = cnt.p + which;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceSelect::If(tmp, bytes, it, out, nsel, n, pred, s);
+        });
+    }
+    int64_t h[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    g.n_lo = h[0];
+    g.n_hi = h[1];
+    if (g.n_hi > 1) {  // descending degree
+        DevBuf<int64_t> dk, dk2;
+        DevBuf<int32_t> v2;
+        dk.alloc(g.n_hi);
+        dk2.alloc(g.n_hi);
+        v2.alloc(g.n_hi);
+        k_bin_degrees<<<grid_for(g.n_hi, kT), kT, 0, s>>>(g.off(), g.bin_hi.p, g.n_hi, dk.p);
+        int64_t *k1 = dk.p, *k2 = dk2.p;
+        int32_t *v1 = g.bin_hi.p, *vv2 = v2.p;
+        int64_t nh = g.n_hi;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k1, k2, v1, vv2, nh, 0, 64, s);
+        });
+        CUDA_TRY(cudaMemcpyAsync(g.bin_hi.p, v2.p, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    g.bin_thr = cfg->degree_threshold;
+    g.bin_single = single;
+}
+
+// Unique canonical pairs (a<=b, sorted) + merged float64 weights -> CSR:
+// emit both arc directions (self-loop once, graph.py:131-134), sort arcs by
+// (src, dst) (graph.py:135-136), offsets by binary search, cast weights.
+template <class W>
+static void assemble_pairs_t(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &pairs, int64_t np, DevBuf<double> &wsum,
+                             int end_bit, DevBuf<W> &out_w) {
+    cudaStream_t s = ctx->stream;
+    DeviceGraph &g = ctx->g;
+    DevBuf<int64_t> arity, posn;
+    arity.alloc(np + 1);
+    posn.alloc(np + 1);
+    CUDA_TRY(cudaMemsetAsync(arity.p, 0, (np + 1) * sizeof(int64_t), s));
+    if (np > 0) k_pair_arity<<<grid_for(np, kT), kT, 0, s>>>(pairs.p, np, arity.p);
+    {
+        int64_t *ain = arity.p, *aout = posn.p;
+        int64_t nn = np + 1;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceScan::ExclusiveSum(tmp, bytes, ain, aout, nn, s); });
+    }
+    int64_t m = 0;
+    CUDA_TRY(cudaMemcpyAsync(&m, posn.p + np, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    arity.release();
+    DevBuf<uint64_t> akeys, akeys2;
+    DevBuf<W> aw;
+    akeys.alloc(m);
+    aw.alloc(m);
+    if (np > 0) k_emit_arcs<W><<<grid_for(np, kT), kT, 0, s>>>(pairs.p, wsum.p, posn.p, np, akeys.p, aw.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    pairs.release();
+    wsum.release();
+    posn.release();
+    akeys2.alloc(m);
+    out_w.alloc(m);
+    {
+        uint64_t *k1 = akeys.p, *k2 = akeys2.p;
+        W *v1 = aw.p, *v2 = out_w.p;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, v1, v2, m, 0, end_bit, s);
+        });
+    }
+    akeys.release();
+    aw.release();
+    g.base.n = n;
+    g.base.m = m;
+    g.base.off.alloc(n + 1);
+    g.base.tgt.alloc(m);
+    k_offsets_from_keys<<<grid_for(n + 1, kT), kT, 0, s>>>(akeys2.p, m, n, g.base.off.p);
+    if (m > 0) k_low32<<<grid_for(m, kT), kT, 0, s>>>(akeys2.p, m, g.base.tgt.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    akeys2.release();
+    g.n = n;
+    g.m = m;
+    g.perm.release();
+    g.ids.release();
+    g.pos.release();
+    g.has_order = 0;
+    ctx->wb.scratch.release();
+}
+
+static void assemble_pairs(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &pairs, int64_t np, DevBuf<double> &wsum,
+                           int end_bit, int w_f64) {
+    ctx->g.base.release();
+    ctx->g.w_f64 = w_f64 ? 1 : 0;
+    if (w_f64) assemble_pairs_t<double>(ctx, n, pairs, np, wsum, end_bit, ctx->g.base.w64);
+    else assemble_pairs_t<float>(ctx, n, pairs, np, wsum, end_bit, ctx->g.base.w32);
+}
+
+// Unit-weight edge keys (min<<32|max, `drop` = removed): sort, run-length
+// encode (duplicate count = merged weight, exact in any order), assemble.
+static void assemble_from_keys(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &keys, int64_t ne, int end_bit) {
+    cudaStream_t s = ctx->stream;
+    DevBuf<uint64_t> sorted;
+    sorted.alloc(ne);
+    {
+        uint64_t *kin = keys.p, *kout = sorted.p;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRadixSort::SortKeys(tmp, bytes, kin, kout, ne, 0, end_bit, s);
+        });
+    }
+    DevBuf<uint32_t> counts;
+    DevBuf<int64_t> nruns;
+    counts.alloc(ne);
+    nruns.alloc(1);
+    {
+        uint64_t *kin = sorted.p, *uniq = keys.p;
+        uint32_t *cnt = counts.p;
+        int64_t *nr = nruns.p;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRunLengthEncode::Encode(tmp, bytes, kin, uniq, cnt, nr, ne, s);
+        });
+    }
+    int64_t np = 0;
+    CUDA_TRY(cudaMemcpyAsync(&np, nruns.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (np > 0) {  // the drop sentinel sorts last
+        uint64_t last = 0;
+        CUDA_TRY(cudaMemcpyAsync(&last, keys.p + np - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if ((last >> 32) >= (uint64_t)n) --np;
+    }
+    sorted.release();
+    DevBuf<double> wsum;
+    wsum.alloc(np);
+    if (np > 0) k_counts_to_double<<<grid_for(np, kT), kT, 0, s>>>(counts.p, np, wsum.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    counts.release();
+    assemble_pairs(ctx, n, keys, np, wsum, end_bit, 0);
+}
+
+static int key_end_bit(int64_t n) { return 32 + ceil_log2((uint64_t)(n > 1 ? n : 2)) + 1; }
+static uint64_t drop_key(int64_t n) { return 1ULL << (key_end_bit(n) - 1); }
+
+void slpa_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                        uint64_t seed, int32_t permute, uint64_t perm_key) {
+    SLPA_REQUIRE(scale >= 1 && scale <= 31, SLPA_EINVAL, "rmat scale must be in [1, 31]");
+    SLPA_REQUIRE(num_edges >= 0, SLPA_EINVAL, "num_edges must be non-negative");
+    const int64_t n = 1LL << scale;
+    DevBuf<uint64_t> keys;
+    keys.alloc(num_edges);
+    if (num_edges > 0)
+        k_gen_rmat<<<grid_for(num_edges, kT), kT, 0, ctx->stream>>>(scale, 0, num_edges, tA, tAB, tABC, seed, permute,
+                                                                    perm_key, drop_key(n), keys.p);
+    CUDA_TRY(cudaGetLastError());
+    assemble_from_keys(ctx, n, keys, num_edges, key_end_bit(n));
+}
+
+void slpa_gen_grid_impl(slpa_ctx *ctx, int64_t rows, int64_t cols, int32_t permute, uint64_t perm_key) {
+    SLPA_REQUIRE(rows >= 1 && cols >= 1 && rows * cols < (1LL << 31), SLPA_EINVAL, "bad grid shape");
+    const int64_t n = rows * cols;
+    DevBuf<uint64_t> keys;
+    keys.alloc(2 * n);
+    k_gen_grid<<<grid_for(2 * n, kT), kT, 0, ctx->stream>>>(rows, cols, permute, perm_key, ceil_log2((uint64_t)n),
+                                                             drop_key(n), keys.p);
+    CUDA_TRY(cudaGetLastError());
+    assemble_from_keys(ctx, n, keys, 2 * n, key_end_bit(n));
+}
+
+void slpa_gen_kmer_impl(slpa_ctx *ctx, int64_t n, uint32_t keep, uint64_t seed, int32_t permute, uint64_t perm_key) {
+    SLPA_REQUIRE(n >= 2 && n < (1LL << 31), SLPA_EINVAL, "bad k-mer graph size");
+    const int64_t ne = (n - 1) + n / 20;
+    DevBuf<uint64_t> keys;
+    keys.alloc(ne);
+    k_gen_kmer<<<grid_for(ne, kT), kT, 0, ctx->stream>>>(n, keep, seed, permute, perm_key, ceil_log2((uint64_t)n),
+                                                          drop_key(n), keys.p);
+    CUDA_TRY(cudaGetLastError());
+    assemble_from_keys(ctx, n, keys, ne, key_end_bit(n));
+}
+
+// build_graph (graph.py:142-162) on the device: canonical pairs, stable sort,
+// float64 duplicate sums in reduceat order, both directions, sorted rows.
+void slpa_build_graph_impl(slpa_ctx *ctx, int64_t n, int64_t ne, const int64_t *src, const int64_t *dst,
+                           const double *w, int32_t weights_f64) {
+    SLPA_REQUIRE(n >= 0 && n < (1LL << 31) - 1 && ne >= 0, SLPA_EINVAL, "bad graph size");
+    for (int64_t i = 0; i < ne; ++i) {
+        SLPA_REQUIRE(src[i] >= 0 && src[i] < n && dst[i] >= 0 && dst[i] < n, SLPA_EINVAL, "edge out of range");
+        if (w) SLPA_REQUIRE(w[i] > 0 && std::isfinite(w[i]), SLPA_EINVAL, "edge must have a positive finite weight");
+    }
+    cudaStream_t s = ctx->stream;
+    const int end_bit = key_end_bit(n);
+    DevBuf<int64_t> d_src, d_dst, idx, idx2;
+    DevBuf<uint64_t> keys, keys2;
+    DevBuf<double> d_w;
+    d_src.alloc(ne);
+    d_dst.alloc(ne);
+    d_w.alloc(ne);
+    keys.alloc(ne);
+    keys2.alloc(ne);
+    idx.alloc(ne);
+    idx2.alloc(ne);
+    if (ne > 0) {
+        CUDA_TRY(cudaMemcpyAsync(d_src.p, src, ne * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(d_dst.p, dst, ne * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        if (w) {
+            CUDA_TRY(cudaMemcpyAsync(d_w.p, w, ne * sizeof(double), cudaMemcpyHostToDevice, s));
+        } else {
+            std::vector<double> ones((size_t)ne, 1.0);
+            CUDA_TRY(cudaMemcpyAsync(d_w.p, ones.data(), ne * sizeof(double), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        k_pair_keys<<<grid_for(ne, kT), kT, 0, s>>>(d_src.p, d_dst.p, ne, keys.p, idx.p);
+        CUDA_TRY(cudaGetLastError());
+        uint64_t *k1 = keys.p, *k2 = keys2.p;
+        int64_t *v1 = idx.p, *v2 = idx2.p;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {  // stable, like np.lexsort
+            return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, v1, v2, ne, 0, end_bit, s);
+        });
+    }
+    d_src.release();
+    d_dst.release();
+    DevBuf<uint32_t> counts;
+    DevBuf<int64_t> nruns, starts;
+    counts.alloc(ne);
+    nruns.alloc(1);
+    CUDA_TRY(cudaMemsetAsync(nruns.p, 0, sizeof(int64_t), s));
+    if (ne > 0) {
+        uint64_t *kin = keys2.p, *uniq = keys.p;
+        uint32_t *cnt = counts.p;
+        int64_t *nr = nruns.p;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRunLengthEncode::Encode(tmp, bytes, kin, uniq, cnt, nr, ne, s);
+        });
+    }
+    int64_t np = 0;
+    CUDA_TRY(cudaMemcpyAsync(&np, nruns.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    starts.alloc(np + 1);
+    DevBuf<double> wsum;
+    wsum.alloc(np);
+    if (np > 0) {
+        DevBuf<int64_t> c64;
+        c64.alloc(np);
+        // exclusive scan of run lengths -> run starts
+        uint32_t *cin = counts.p;
+        int64_t *sout = starts.p;
+        int64_t nn = np;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceScan::ExclusiveSum(tmp, bytes, cin, sout, nn, s); });
+        k_run_sums<<<grid_for(np, kT), kT, 0, s>>>(d_w.p, idx2.p, starts.p, counts.p, np, wsum.p);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    keys2.release();
+    idx.release();
+    idx2.release();
+    d_w.release();
+    counts.release();
+    starts.release();
+    assemble_pairs(ctx, n, keys, np, wsum, end_bit, weights_f64);
+}

@@ -1,0 +1,191 @@
+// slpa_internal.cuh -- shared declarations of the B200 label-propagation engine.
+//
+// Device data layout (per context, HBM):
+//   CSR        off int64[n+1] | tgt int32[m] | w float32|float64[m]   (visiting order)
+//   ids        int32[n]   position -> original vertex id (label value); null = identity
+//   cls        uint8[n]   degree class for the current threshold (0 none, 1 low, 2 high)
+//   bins       int32[n_lo] low-degree positions (ascending) | int32[n_hi] high-degree (degree desc)
+//   lab_old    int32[n]   labels at the start of the sweep (L0)
+//   lab_new    uint32[n]  speculative end-of-sweep labels, bit 31 = "changed" (L1 | chg<<31)
+//   flag_cur   uint8[n]   unprocessed flags at the start of the sweep (F0)
+//   flag_next  uint8[n]   unprocessed flags produced by this sweep (F1)
+//   dirty[2]   uint32[ceil(n/32)] re-evaluation bitmaps (next round)
+//   wl_lo/hi   int32[n]   round worklists
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include "../../include/slpa.h"
+
+#define SLPA_CHG 0x80000000u
+#define SLPA_LMASK 0x7fffffffu
+#define SLPA_KDYN 64          // max sketch slots on the dynamic-k path
+#define SLPA_KHI_MAX 32       // slot-parallel merge holds one slot per lane
+
+enum { CLS_NONE = 0, CLS_LO = 1, CLS_HI = 2 };
+
+struct SlpaError {
+    int32_t code;
+    std::string msg;
+};
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            throw SlpaError{SLPA_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+    } while (0)
+
+#define SLPA_REQUIRE(cond, code, msg) \
+    do {                              \
+        if (!(cond)) throw SlpaError{(code), (msg)}; \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t count = 0;
+    void alloc(size_t c) {
+        if (c <= count && p) return;
+        release();
+        if (c == 0) c = 1;
+        CUDA_TRY(cudaMalloc((void **)&p, c * sizeof(T)));
+        count = c;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    size_t bytes() const { return p ? count * sizeof(T) : 0; }
+};
+
+// Arguments shared by every sweep kernel (passed by value).
+struct SweepArgs {
+    const int64_t *__restrict__ off;
+    const int32_t *__restrict__ tgt;
+    const void *__restrict__ w;      // float or double, by template
+    const int64_t *__restrict__ roff; // reverse CSR (asymmetric graphs only)
+    const int32_t *__restrict__ rsrc;
+    const uint8_t *__restrict__ cls;
+    int32_t *lab_old;                 // det: L0 (read-only in rounds) ; async: the in-place labels
+    uint32_t *lab_new;                // det only
+    uint8_t *flag_cur;
+    uint8_t *flag_next;
+    uint32_t *dirty_next;             // det: bitmap for the next round
+    unsigned long long *counters;     // [0] lo count, [1] hi count, [2] delta, [3] evals, [4] arcs
+    int32_t pickless;
+    int32_t k;                        // sketch slots
+    int32_t parts;                    // partial_groups
+    int32_t scan_double;
+    int32_t symmetric;
+};
+
+enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_N = 8 };
+#define CNT_STRIPES 64
+#define CNT_TOTAL (CNT_N * CNT_STRIPES)
+
+struct Csr {
+    int64_t n = 0, m = 0;
+    DevBuf<int64_t> off;
+    DevBuf<int32_t> tgt;
+    DevBuf<float> w32;
+    DevBuf<double> w64;
+    void release() { off.release(); tgt.release(); w32.release(); w64.release(); n = m = 0; }
+    size_t bytes() const { return off.bytes() + tgt.bytes() + w32.bytes() + w64.bytes(); }
+};
+
+struct DeviceGraph {
+    int64_t n = 0, m = 0;
+    int32_t w_f64 = 0;
+    int32_t symmetric = 1;
+    int32_t has_order = 0;
+    Csr base;              // original ids (as uploaded / generated)
+    Csr perm;              // visiting-order positions (has_order only)
+    DevBuf<int32_t> ids;   // position -> id (has_order)
+    DevBuf<int32_t> pos;   // id -> position (has_order)
+    DevBuf<int64_t> roff;  // reverse CSR of the active numbering (!symmetric)
+    DevBuf<int32_t> rsrc;
+    // degree bins (per threshold)
+    int32_t bin_thr = -1;
+    int32_t bin_single = -1;  // all non-empty vertices in the low bin (exact / shared sketch)
+    DevBuf<uint8_t> cls;
+    DevBuf<int32_t> bin_lo, bin_hi;
+    int64_t n_lo = 0, n_hi = 0;
+    const Csr &act() const { return has_order ? perm : base; }
+    const int64_t *off() const { return act().off.p; }
+    const int32_t *tgt() const { return act().tgt.p; }
+    const void *w() const { return w_f64 ? (const void *)act().w64.p : (const void *)act().w32.p; }
+    size_t bytes() const {
+        return base.bytes() + perm.bytes() + ids.bytes() + pos.bytes() + roff.bytes() + rsrc.bytes() + cls.bytes() +
+               bin_lo.bytes() + bin_hi.bytes();
+    }
+    size_t csr_bytes() const { return act().bytes(); }
+};
+
+struct WorkBuffers {
+    DevBuf<int32_t> lab_old;
+    DevBuf<uint32_t> lab_new;
+    DevBuf<uint8_t> flag_a, flag_b;
+    DevBuf<uint32_t> dirty_a, dirty_b;
+    DevBuf<int32_t> wl_lo, wl_hi;
+    DevBuf<int32_t> io_labels;  // staging for host <-> device label exchange
+    DevBuf<uint8_t> io_flags;
+    DevBuf<unsigned long long> counters;
+    DevBuf<double> metric_d;    // tallies for modularity
+    DevBuf<unsigned long long> metric_u;
+    DevBuf<unsigned char> scratch;  // cub temp storage
+    size_t bytes() const {
+        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() +
+               dirty_b.bytes() + wl_lo.bytes() + wl_hi.bytes() + io_labels.bytes() + io_flags.bytes() +
+               counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
+    }
+};
+
+struct slpa_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    DeviceGraph g;
+    WorkBuffers wb;
+    unsigned long long *h_counters = nullptr;  // pinned mirror of wb.counters (striped)
+    unsigned long long h_sum[CNT_N] = {};      // per-counter sums of the stripes
+    std::string err;
+    slpa_run_stats stats{};
+    int32_t prof_on = 0;
+    slpa_profile prof{};
+    cudaEvent_t pev0 = nullptr, pev1 = nullptr;
+    int32_t have_labels = 0;   // lab_old holds labels of a finished run
+    // multi-GPU partition
+    int32_t part = 0;
+    int64_t v_begin = 0, v_end = 0;
+};
+
+// ---------------------------------------------------------------- host-side helpers
+void slpa_validate_config(const slpa_config *cfg);
+void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg);
+void slpa_graph_finalize(slpa_ctx *ctx);  // symmetry check, reverse CSR, reset bins
+void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order_host_or_dev, bool on_device);
+void slpa_alloc_work(slpa_ctx *ctx);
+void slpa_assemble_unit_edges(slpa_ctx *ctx, int64_t n, int64_t num_edges, uint32_t *d_src, uint32_t *d_dst);
+
+// sweep drivers (slpa_sweep.cu)
+int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless);
+int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless);
+void slpa_init_labels(slpa_ctx *ctx);  // lab = ids (or arange), flags = 1
+void slpa_labels_to_host(slpa_ctx *ctx, int32_t *host);       // by original id
+void slpa_labels_from_host(slpa_ctx *ctx, const int32_t *host);
+void slpa_flags_to_host(slpa_ctx *ctx, uint8_t *host);
+void slpa_flags_from_host(slpa_ctx *ctx, const uint8_t *host);
+void slpa_permute_id_to_pos(slpa_ctx *ctx, const int32_t *d_by_id, int32_t *d_by_pos);
+
+// metrics (slpa_metrics.cu)
+void slpa_tally(slpa_ctx *ctx, const int32_t *d_labels_by_pos, double *q, int64_t *ncomm, int64_t *sizes,
+                double *internal, double *incident);
+
+static inline unsigned grid_for(int64_t count, int threads) {
+    int64_t b = (count + threads - 1) / threads;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}

@@ -1,0 +1,834 @@
+// slpa_sweep.cu -- one label-propagation sweep on the B200.
+//
+// Reference semantics (lpa.py:204-224): vertices are visited in order; an
+// unprocessed vertex clears its flag, selects a candidate from its
+// neighbours' CURRENT labels (earlier vertices' updates of this sweep are
+// visible), adopts it when it differs (and, in pick-less sweeps, is
+// smaller), and then marks all its out-neighbours unprocessed.
+//
+// Deterministic mode (worker_count == 0) reproduces that sequential sweep
+// bit-exactly with speculative rounds:
+//   * vertex v's inputs are L1[u] of lower-positioned neighbours u (the
+//     labels they end the sweep with) and L0[u] of higher ones;
+//   * v takes its turn iff F0[v] or some lower in-neighbour changed;
+//   * the map (inputs -> output) is acyclic in position, so its fixpoint is
+//     unique and equals the sequential sweep.  Round 0 evaluates every
+//     flagged vertex against the current estimates; any vertex whose output
+//     (label, changed bit) moves re-queues its higher-positioned dependants
+//     (dirty bitmap); rounds repeat until no output moves.
+//   * L1 and the changed bit share one 32-bit word (bit 31), so a single
+//     gather of a lower neighbour gives its label and whether it changed.
+// Async mode (worker_count > 0) is the paper's in-place parallel sweep.
+#include "slpa_sketch.cuh"
+#include "slpa_internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ label reads
+// Deterministic mode: neighbour t of v (positions).  Lower neighbours give
+// L1 (speculative, possibly written this round -> L2 load), higher ones L0.
+__device__ __forceinline__ int32_t det_label(const SweepArgs &a, int32_t t, int32_t v, bool &lower_changed) {
+    if (t < v) {
+        uint32_t L = __ldcg(&a.lab_new[t]);
+        lower_changed |= (L >> 31) != 0;
+        return (int32_t)(L & SLPA_LMASK);
+    }
+    return __ldg(&a.lab_old[t]);
+}
+
+__device__ __forceinline__ int32_t async_label(const SweepArgs &a, int32_t t) { return __ldcg(&a.lab_old[t]); }
+
+template <class W>
+__device__ __forceinline__ double arc_weight(const SweepArgs &a, int64_t e) {
+    return (double)__ldg(reinterpret_cast<const W *>(a.w) + e);
+}
+
+// T for an asymmetric graph: some lower in-neighbour changed.
+__device__ __forceinline__ bool lower_in_changed(const SweepArgs &a, int32_t v) {
+    for (int64_t e = a.roff[v]; e < a.roff[v + 1]; ++e) {
+        int32_t u = a.rsrc[e];
+        if (u < v && (__ldcg(&a.lab_new[u]) >> 31)) return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ void mark_dirty(uint32_t *bm, int32_t t) { atomicOr(&bm[t >> 5], 1u << (t & 31)); }
+
+// Re-queue v's higher-positioned dependants (readers of v's label and
+// vertices whose turn depends on v's changed bit).
+__device__ __forceinline__ void mark_dependants(const SweepArgs &a, int32_t v, int64_t lo, int64_t hi, int start,
+                                                int stride) {
+    for (int64_t e = lo + start; e < hi; e += stride) {
+        int32_t t = __ldg(&a.tgt[e]);
+        if (t > v) mark_dirty(a.dirty_next, t);
+    }
+    if (!a.symmetric) {
+        for (int64_t e = a.roff[v] + start; e < a.roff[v + 1]; e += stride) {
+            int32_t u = a.rsrc[e];
+            if (u > v) mark_dirty(a.dirty_next, u);
+        }
+    }
+}
+
+// Counters are striped over CNT_STRIPES slots (by warp) so that per-warp
+// atomics do not serialise on one L2 address; the host sums the stripes.
+__device__ __forceinline__ int stripe() {
+    return (int)((((unsigned)blockIdx.x * blockDim.x + threadIdx.x) >> 5) & (CNT_STRIPES - 1));
+}
+__device__ __forceinline__ void ctr_add(unsigned long long *ctr, int which, unsigned long long x) {
+    atomicAdd(&ctr[which * CNT_STRIPES + stripe()], x);
+}
+
+// Warp-aggregated counter update; every lane of the warp must call it.
+__device__ __forceinline__ void warp_count(unsigned long long *ctr, unsigned long long evals,
+                                           unsigned long long arcs, unsigned long long delta) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        evals += __shfl_xor_sync(0xffffffffu, evals, o);
+        arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
+        delta += __shfl_xor_sync(0xffffffffu, delta, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        const int s = stripe();
+        if (evals) atomicAdd(&ctr[CNT_EVALS * CNT_STRIPES + s], evals);
+        if (arcs) atomicAdd(&ctr[CNT_ARCS * CNT_STRIPES + s], arcs);
+        if (delta) atomicAdd(&ctr[CNT_DELTA * CNT_STRIPES + s], delta);
+    }
+}
+
+// Finish one deterministic evaluation (thread-per-vertex flavour).
+__device__ __forceinline__ void det_commit_output(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand, bool T,
+                                                  int64_t lo, int64_t hi) {
+    bool chg = T && cand != cur && (!a.pickless || cand < cur);
+    uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
+    uint32_t ow = __ldcg(&a.lab_new[v]);
+    if (nw != ow) {
+        __stcg(&a.lab_new[v], nw);
+        mark_dependants(a, v, lo, hi, 0, 1);
+    }
+}
+
+__device__ __forceinline__ void async_commit_output(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand,
+                                                    int64_t lo, int64_t hi, unsigned long long &delta) {
+    if (cand != cur && (!a.pickless || cand < cur)) {
+        __stcg(&a.lab_old[v], cand);
+        delta = 1;
+        for (int64_t e = lo; e < hi; ++e) a.flag_cur[__ldg(&a.tgt[e])] = 1;
+    }
+}
+
+// Finish one evaluation in a warp-per-vertex kernel (all lanes call it with
+// warp-uniform arguments except lower_changed).
+template <bool DET>
+__device__ __forceinline__ void warp_hi_finish(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand, uint8_t f0,
+                                               bool lower_changed, int64_t lo, int64_t hi, int lane) {
+    if (DET) {
+        bool T = f0 != 0;
+        if (!T) T = a.symmetric ? __any_sync(0xffffffffu, lower_changed) : lower_in_changed(a, v);
+        bool chg = T && cand != cur && (!a.pickless || cand < cur);
+        uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
+        uint32_t ow = __ldcg(&a.lab_new[v]);
+        __syncwarp();
+        if (nw != ow) {
+            if (lane == 0) __stcg(&a.lab_new[v], nw);
+            mark_dependants(a, v, lo, hi, lane, 32);
+        }
+        if (lane == 0) {
+            ctr_add(a.counters, CNT_EVALS_HI, 1ull);
+            ctr_add(a.counters, CNT_ARCS_HI, (unsigned long long)(hi - lo));
+        }
+    } else {
+        if (cand != cur && (!a.pickless || cand < cur)) {
+            if (lane == 0) {
+                __stcg(&a.lab_old[v], cand);
+                ctr_add(a.counters, CNT_DELTA, 1ull);
+            }
+            for (int64_t e = lo + lane; e < hi; e += 32) a.flag_cur[__ldg(&a.tgt[e])] = 1;
+        }
+        if (lane == 0) {
+            ctr_add(a.counters, CNT_EVALS_HI, 1ull);
+            ctr_add(a.counters, CNT_ARCS_HI, (unsigned long long)(hi - lo));
+        }
+    }
+}
+
+// ================================================================== MG, low degree
+// One thread per vertex, one register-resident k-slot sketch over the
+// non-self arcs in adjacency order (lpa.py:173-177), optional rescan
+// (lpa.py:187-191), max_key or the current label (lpa.py:192-193).
+// No early returns: every lane reaches the warp-aggregated counters.
+template <class W, int K, bool DET>
+__global__ void __launch_bounds__(kThreads) k_mg_lo(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                    int round0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
+    int32_t v = 0;
+    uint8_t f0 = 0;
+    bool go = false;
+    if (i < count) {
+        v = __ldg(&list[i]);
+        f0 = a.flag_cur[v];
+        go = DET ? (!round0 || f0) : (f0 != 0);
+    }
+    if (go) {
+        if (!DET) a.flag_cur[v] = 0;
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+        const int k = K > 0 ? K : a.k;
+        bool lower_changed = false;
+        MgSketchDev<K> sk;
+        sk.reset(k);
+        for (int64_t e = lo; e < hi; ++e) {
+            int32_t t = __ldg(&a.tgt[e]);
+            if (t == v) continue;
+            int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
+            sk.acc(c, arc_weight<W>(a, e), k);
+        }
+        if (a.scan_double) {
+            sk.clear_values(k);
+            bool dummy = false;
+            for (int64_t e = lo; e < hi; ++e) {
+                int32_t t = __ldg(&a.tgt[e]);
+                if (t == v) continue;
+                int32_t c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
+                sk.rescan_add(c, arc_weight<W>(a, e), k);
+            }
+        }
+        int32_t best;
+        const int32_t cand = sk.max_key(k, best) ? best : cur;
+        n_eval = 1;
+        n_arcs = (unsigned long long)(hi - lo);
+        if (DET) {
+            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
+            det_commit_output(a, v, cur, cand, T, lo, hi);
+        } else {
+            async_commit_output(a, v, cur, cand, lo, hi, n_delta);
+        }
+    }
+    warp_count(a.counters, n_eval, n_arcs, n_delta);
+}
+
+// ================================================================== MG, high degree
+// One warp per vertex.  Lane g owns chunk g of _chunk_bounds(deg, R_H)
+// (lpa.py:178-183) and a register sketch; parts are then merged into
+// parts[0] in order, replaying each part's non-empty slots ascending
+// (sketch.py:76-91), on a slot-parallel warp sketch (lane l = slot l).
+template <class W, int K, bool DET>
+__global__ void __launch_bounds__(kThreads) k_mg_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                    int round0) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;  // warp-uniform
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int k = K > 0 ? K : a.k;
+    const int P = a.parts;
+    bool lower_changed = false;
+    WarpSketch S{0, 0.0};
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        MgSketchDev<K> part;
+        part.reset(k);
+        if (p < P) {
+            int64_t s, e;
+            chunk_bounds(deg, P, p, s, e);
+            for (int64_t x = lo + s; x < lo + e; ++x) {
+                int32_t t = __ldg(&a.tgt[x]);
+                if (t == v) continue;
+                int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
+                part.acc(c, arc_weight<W>(a, x), k);
+            }
+        }
+        int first = 0;
+        if (b0 == 0) {  // sk = parts[0]
+#pragma unroll
+            for (int i = 0; i < KArr<K>::v; ++i) {
+                if (K == 0 && i >= k) break;
+                int32_t kk = __shfl_sync(0xffffffffu, part.key[i], 0);
+                double vv = __shfl_sync(0xffffffffu, part.val[i], 0);
+                if (lane == i) { S.key = kk; S.val = vv; }
+            }
+            first = 1;
+        }
+        const int nb = min(32, P - b0);
+        for (int q = first; q < nb; ++q) {
+#pragma unroll
+            for (int i = 0; i < KArr<K>::v; ++i) {
+                if (K == 0 && i >= k) break;
+                int32_t c = __shfl_sync(0xffffffffu, part.key[i], q);
+                double w = __shfl_sync(0xffffffffu, part.val[i], q);
+                if (w > 0.0) S.acc(lane, k, c, w);
+            }
+        }
+    }
+    if (a.scan_double) {  // exact per-key re-count in adjacency order
+        S.val = 0.0;
+        bool dummy = false;
+        for (int64_t base = lo; base < hi; base += 32) {
+            int64_t x = base + lane;
+            int32_t c = 0;
+            double w = 0.0;
+            bool ok = false;
+            if (x < hi) {
+                int32_t t = __ldg(&a.tgt[x]);
+                if (t != v) {
+                    ok = true;
+                    c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
+                    w = arc_weight<W>(a, x);
+                }
+            }
+            unsigned okm = __ballot_sync(0xffffffffu, ok);
+            while (okm) {
+                int j = __ffs(okm) - 1;
+                okm &= okm - 1;
+                int32_t cj = __shfl_sync(0xffffffffu, c, j);
+                double wj = __shfl_sync(0xffffffffu, w, j);
+                S.rescan_add(lane, k, cj, wj);
+            }
+        }
+    }
+    int32_t best;
+    const bool found = S.max_key(lane, k, best);
+    const int32_t cand = found ? best : cur;
+    warp_hi_finish<DET>(a, v, cur, cand, f0, lower_changed, lo, hi, lane);
+}
+
+// ================================================================== BM
+// Low degree: one BmState(cur, 0.0) over the non-self arcs (lpa.py:137-142).
+template <class W, bool DET>
+__global__ void __launch_bounds__(kThreads) k_bm_lo(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                    int round0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
+    int32_t v = 0;
+    uint8_t f0 = 0;
+    bool go = false;
+    if (i < count) {
+        v = __ldg(&list[i]);
+        f0 = a.flag_cur[v];
+        go = DET ? (!round0 || f0) : (f0 != 0);
+    }
+    if (go) {
+        if (!DET) a.flag_cur[v] = 0;
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+        bool lower_changed = false;
+        BmVote st{cur, 0.0};
+        for (int64_t e = lo; e < hi; ++e) {
+            int32_t t = __ldg(&a.tgt[e]);
+            if (t == v) continue;
+            int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
+            st.acc(c, arc_weight<W>(a, e));
+        }
+        const int32_t cand = st.cand;
+        n_eval = 1;
+        n_arcs = (unsigned long long)(hi - lo);
+        if (DET) {
+            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
+            det_commit_output(a, v, cur, cand, T, lo, hi);
+        } else {
+            async_commit_output(a, v, cur, cand, lo, hi, n_delta);
+        }
+    }
+    warp_count(a.counters, n_eval, n_arcs, n_delta);
+}
+
+// High degree: one vote per chunk (each starts at (cur, 0)), reduce_votes
+// pair-max -- a total order, so the warp butterfly gives the same answer.
+template <class W, bool DET>
+__global__ void __launch_bounds__(kThreads) k_bm_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                    int round0) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int P = a.parts;
+    bool lower_changed = false;
+    bool have = false;
+    int32_t bc = 0;
+    double bw = 0.0;
+    for (int p = lane; p < P; p += 32) {
+        int64_t s, e;
+        chunk_bounds(deg, P, p, s, e);
+        BmVote st{cur, 0.0};
+        for (int64_t x = lo + s; x < lo + e; ++x) {
+            int32_t t = __ldg(&a.tgt[x]);
+            if (t == v) continue;
+            int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
+            st.acc(c, arc_weight<W>(a, x));
+        }
+        if (!have || bm_better(st.w, st.cand, bw, bc)) { bc = st.cand; bw = st.w; have = true; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+        int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        double ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
+    }
+    warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
+}
+
+// ================================================================== exact
+// select_label_exact (lpa.py:92-107): per-label totals summed in adjacency
+// order (np.bincount order), argmax = smallest label among ties.  One thread
+// per vertex, O(deg^2) -- the correctness path for the quality baseline.
+template <class W, bool DET>
+__global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                    int round0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
+    int32_t v = 0;
+    uint8_t f0 = 0;
+    bool go = false;
+    if (i < count) {
+        v = __ldg(&list[i]);
+        f0 = a.flag_cur[v];
+        go = DET ? (!round0 || f0) : (f0 != 0);
+    }
+    if (go) {
+        if (!DET) a.flag_cur[v] = 0;
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+        bool lower_changed = false, dummy = false;
+        bool found = false;
+        int32_t best = 0;
+        double bw = 0.0;
+        for (int64_t e1 = lo; e1 < hi; ++e1) {
+            int32_t t1 = __ldg(&a.tgt[e1]);
+            if (t1 == v) continue;
+            int32_t c1 = DET ? det_label(a, t1, v, lower_changed) : async_label(a, t1);
+            bool seen = false;
+            for (int64_t e0 = lo; e0 < e1 && !seen; ++e0) {
+                int32_t t0 = __ldg(&a.tgt[e0]);
+                if (t0 == v) continue;
+                int32_t c0 = DET ? det_label(a, t0, v, dummy) : async_label(a, t0);
+                seen = (c0 == c1);
+            }
+            if (seen) continue;
+            double tot = 0.0;
+            for (int64_t e2 = e1; e2 < hi; ++e2) {
+                int32_t t2 = __ldg(&a.tgt[e2]);
+                if (t2 == v) continue;
+                int32_t c2 = DET ? det_label(a, t2, v, dummy) : async_label(a, t2);
+                if (c2 == c1) tot += arc_weight<W>(a, e2);
+            }
+            if (!found || tot > bw || (tot == bw && c1 < best)) { best = c1; bw = tot; found = true; }
+        }
+        const int32_t cand = found ? best : cur;
+        n_eval = 1;
+        n_arcs = (unsigned long long)(hi - lo);
+        if (DET) {
+            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
+            det_commit_output(a, v, cur, cand, T, lo, hi);
+        } else {
+            async_commit_output(a, v, cur, cand, lo, hi, n_delta);
+        }
+    }
+    warp_count(a.counters, n_eval, n_arcs, n_delta);
+}
+
+// ================================================================== round plumbing
+// Dirty bitmap -> next-round worklists, split by degree class; consumed
+// words are cleared so the same bitmap collects the following round.
+__global__ void __launch_bounds__(kThreads) k_compact(uint32_t *__restrict__ dirty, int64_t nwords,
+                                                      const uint8_t *__restrict__ cls, int32_t *__restrict__ wl_lo,
+                                                      int32_t *__restrict__ wl_hi,
+                                                      unsigned long long *__restrict__ counters) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t word = 0;
+    if (i < nwords) {
+        word = dirty[i];
+        if (word) dirty[i] = 0;
+    }
+    int nlo = 0, nhi = 0;
+    for (uint32_t w = word; w; w &= w - 1) {
+        int32_t v = (int32_t)(i * 32 + (__ffs(w) - 1));
+        uint8_t c = cls[v];
+        nlo += c == CLS_LO;
+        nhi += c == CLS_HI;
+    }
+    const int lane = threadIdx.x & 31;
+    int plo = nlo, phi = nhi;  // inclusive scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int a = __shfl_up_sync(0xffffffffu, plo, o);
+        int b = __shfl_up_sync(0xffffffffu, phi, o);
+        if (lane >= o) { plo += a; phi += b; }
+    }
+    unsigned long long blo = 0, bhi = 0;
+    int tlo = __shfl_sync(0xffffffffu, plo, 31), thi = __shfl_sync(0xffffffffu, phi, 31);
+    if (lane == 31) {
+        if (tlo) blo = atomicAdd(&counters[CNT_LO * CNT_STRIPES], (unsigned long long)tlo);
+        if (thi) bhi = atomicAdd(&counters[CNT_HI * CNT_STRIPES], (unsigned long long)thi);
+    }
+    blo = __shfl_sync(0xffffffffu, blo, 31) + (plo - nlo);
+    bhi = __shfl_sync(0xffffffffu, bhi, 31) + (phi - nhi);
+    for (uint32_t w = word; w; w &= w - 1) {
+        int32_t v = (int32_t)(i * 32 + (__ffs(w) - 1));
+        uint8_t c = cls[v];
+        if (c == CLS_LO) wl_lo[blo++] = v;
+        else if (c == CLS_HI) wl_hi[bhi++] = v;
+    }
+}
+
+// End of a deterministic sweep: fold L1 into L0, count ΔN, and set the
+// next sweep's flags: a changed u marks its out-neighbours t with
+// pos(t) <= pos(u) (those whose turn has passed; lpa.py:223).
+__global__ void __launch_bounds__(kThreads) k_commit_lo(SweepArgs a, const int32_t *__restrict__ list, int64_t count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long d = 0;
+    if (i < count) {
+        const int32_t v = __ldg(&list[i]);
+        uint32_t wv = a.lab_new[v];
+        if (wv & SLPA_CHG) {
+            int32_t c = (int32_t)(wv & SLPA_LMASK);
+            a.lab_old[v] = c;
+            a.lab_new[v] = (uint32_t)c;
+            d = 1;
+            const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+            for (int64_t e = lo; e < hi; ++e) {
+                int32_t t = __ldg(&a.tgt[e]);
+                if (t <= v) a.flag_next[t] = 1;
+            }
+        }
+    }
+    warp_count(a.counters, 0, 0, d);
+}
+
+__global__ void __launch_bounds__(kThreads) k_commit_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t v = __ldg(&list[wid]);
+    uint32_t wv = a.lab_new[v];
+    if (!(wv & SLPA_CHG)) return;
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+        int32_t t = __ldg(&a.tgt[e]);
+        if (t <= v) a.flag_next[t] = 1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int32_t c = (int32_t)(wv & SLPA_LMASK);
+        a.lab_old[v] = c;
+        a.lab_new[v] = (uint32_t)c;
+        ctr_add(a.counters, CNT_DELTA, 1ull);
+    }
+}
+
+__global__ void k_init_labels(int32_t *lab_old, uint32_t *lab_new, uint8_t *flags, const int32_t *ids, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t l = ids ? ids[i] : (int32_t)i;
+    lab_old[i] = l;
+    if (lab_new) lab_new[i] = (uint32_t)l;
+    flags[i] = 1;
+}
+
+__global__ void k_clear_isolated_flags(uint8_t *flags, const uint8_t *cls, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && cls[i] == CLS_NONE) flags[i] = 0;
+}
+
+// by-position <-> by-id permutations for host I/O
+__global__ void k_pos_to_id_i32(const int32_t *src, int32_t *dst, const int32_t *ids, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[ids[i]] = src[i];
+}
+__global__ void k_id_to_pos_i32(const int32_t *src, int32_t *dst, const int32_t *ids, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[ids[i]];
+}
+__global__ void k_pos_to_id_u8(const uint8_t *src, uint8_t *dst, const int32_t *ids, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[ids[i]] = src[i];
+}
+__global__ void k_id_to_pos_u8(const uint8_t *src, uint8_t *dst, const int32_t *ids, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[ids[i]] ? 1 : 0;
+}
+__global__ void k_norm_flags(uint8_t *f, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) f[i] = f[i] ? 1 : 0;
+}
+__global__ void k_sync_lab_new(const int32_t *lab_old, uint32_t *lab_new, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) lab_new[i] = (uint32_t)lab_old[i];
+}
+
+// ------------------------------------------------------------------ dispatch
+typedef void (*EvalKernel)(SweepArgs, const int32_t *, int64_t, int);
+
+struct KernelPair {
+    EvalKernel lo, hi;
+    bool hi_is_warp;
+};
+
+template <class W, bool DET>
+KernelPair pick_kernels(const slpa_config *cfg) {
+    if (cfg->variant == SLPA_VARIANT_EXACT) return {k_exact<W, DET>, k_exact<W, DET>, false};
+    if (cfg->variant == SLPA_VARIANT_BM) return {k_bm_lo<W, DET>, k_bm_hi<W, DET>, true};
+    if (cfg->sketch_slots == 8) return {k_mg_lo<W, 8, DET>, k_mg_hi<W, 8, DET>, true};
+    return {k_mg_lo<W, 0, DET>, k_mg_hi<W, 0, DET>, true};
+}
+
+KernelPair kernels_for(const slpa_ctx *ctx, const slpa_config *cfg, bool det) {
+    if (ctx->g.w_f64) return det ? pick_kernels<double, true>(cfg) : pick_kernels<double, false>(cfg);
+    return det ? pick_kernels<float, true>(cfg) : pick_kernels<float, false>(cfg);
+}
+
+SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
+    SweepArgs a{};
+    DeviceGraph &g = ctx->g;
+    a.off = g.off();
+    a.tgt = g.tgt();
+    a.w = g.w();
+    a.roff = g.symmetric ? nullptr : g.roff.p;
+    a.rsrc = g.symmetric ? nullptr : g.rsrc.p;
+    a.cls = g.cls.p;
+    a.lab_old = ctx->wb.lab_old.p;
+    a.lab_new = ctx->wb.lab_new.p;
+    a.flag_cur = ctx->wb.flag_a.p;
+    a.flag_next = ctx->wb.flag_b.p;
+    a.dirty_next = ctx->wb.dirty_a.p;
+    a.counters = ctx->wb.counters.p;
+    a.pickless = pickless;
+    a.k = cfg->sketch_slots;
+    a.parts = cfg->partial_groups;
+    a.scan_double = cfg->scan_mode == SLPA_SCAN_DOUBLE;
+    a.symmetric = g.symmetric;
+    return a;
+}
+
+void read_counters(slpa_ctx *ctx) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, ctx->wb.counters.p, CNT_TOTAL * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < CNT_N; ++c) {
+        unsigned long long s = 0;
+        for (int j = 0; j < CNT_STRIPES; ++j) s += ctx->h_counters[c * CNT_STRIPES + j];
+        ctx->h_sum[c] = s;
+    }
+}
+
+// Profiling mode (slpa_set_profiling): CUDA events on the context stream
+// around every launch, attributed to a kernel class with the vertices and
+// arcs that launch evaluated.  Off by default (no host syncs added).
+template <class F>
+void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn) {
+    ctx->stats.kernel_launches += nlaunch;
+    if (!ctx->prof_on) {
+        fn();
+        return;
+    }
+    unsigned long long e0 = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
+    unsigned long long a0 = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
+    CUDA_TRY(cudaEventRecord(ctx->pev0, ctx->stream));
+    fn();
+    CUDA_TRY(cudaEventRecord(ctx->pev1, ctx->stream));
+    CUDA_TRY(cudaEventSynchronize(ctx->pev1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ctx->pev0, ctx->pev1));
+    read_counters(ctx);
+    ctx->prof.launches[cls] += nlaunch;
+    ctx->prof.ms[cls] += ms;
+    ctx->prof.evals[cls] += (int64_t)(ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI] - e0);
+    ctx->prof.arcs[cls] += (int64_t)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI] - a0);
+}
+
+void launch_lo(slpa_ctx *ctx, const KernelPair &kp, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
+               int cls) {
+    if (cnt <= 0) return;
+    timed_launch(ctx, cls, 1, [&] {
+        kp.lo<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+        CUDA_TRY(cudaGetLastError());
+    });
+}
+
+void launch_hi(slpa_ctx *ctx, const KernelPair &kp, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
+               int cls) {
+    if (cnt <= 0) return;
+    timed_launch(ctx, cls, 1, [&] {
+        if (kp.hi_is_warp)
+            kp.hi<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+        else
+            kp.hi<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+        CUDA_TRY(cudaGetLastError());
+    });
+}
+
+}  // namespace
+
+// ====================================================================== drivers
+int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
+    DeviceGraph &g = ctx->g;
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = g.n;
+    KernelPair kp = kernels_for(ctx, cfg, true);
+    SweepArgs a = make_args(ctx, cfg, pickless);
+    CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(wb.flag_b.p, 0, (size_t)n, s));
+    for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
+    // round 0: every flagged vertex, straight from the degree bins
+    launch_lo(ctx, kp, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    launch_hi(ctx, kp, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+    int64_t rounds = 1;
+    unsigned long long evals0 = 0, arcs0 = 0;
+    bool first = true;
+    const int64_t nwords = (n + 31) / 32;
+    for (;;) {
+        CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, 2 * CNT_STRIPES * sizeof(unsigned long long), s));
+        timed_launch(ctx, SLPA_PROF_COMPACT, 1, [&] {
+            k_compact<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, nwords, g.cls.p, wb.wl_lo.p,
+                                                                      wb.wl_hi.p, wb.counters.p);
+            CUDA_TRY(cudaGetLastError());
+        });
+        read_counters(ctx);
+        if (first) {
+            evals0 = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
+            arcs0 = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
+            first = false;
+        }
+        const int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nhi = (int64_t)ctx->h_sum[CNT_HI];
+        if (nlo == 0 && nhi == 0) break;
+        launch_hi(ctx, kp, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
+        launch_lo(ctx, kp, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
+        ++rounds;
+    }
+    const unsigned long long evals = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
+    const unsigned long long arcs = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
+    // commit: L0 <- L1, delta, next-sweep flags
+    timed_launch(ctx, SLPA_PROF_COMMIT, (g.n_lo > 0) + (g.n_hi > 0), [&] {
+        if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
+        if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
+        CUDA_TRY(cudaGetLastError());
+    });
+    read_counters(ctx);
+    std::swap(wb.flag_a, wb.flag_b);
+    ctx->stats.rounds += rounds;
+    ctx->stats.vertex_evals += (int64_t)evals;
+    ctx->stats.arc_reads += (int64_t)arcs;
+    ctx->stats.first_evals += (int64_t)evals0;
+    ctx->stats.first_arcs += (int64_t)arcs0;
+    return (int64_t)ctx->h_sum[CNT_DELTA];
+}
+
+int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
+    DeviceGraph &g = ctx->g;
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    KernelPair kp = kernels_for(ctx, cfg, false);
+    SweepArgs a = make_args(ctx, cfg, pickless);
+    CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
+    for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
+    // Higher-degree vertices first: they carry most arcs and the tail.
+    launch_hi(ctx, kp, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+    launch_lo(ctx, kp, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    timed_launch(ctx, SLPA_PROF_OTHER, 1, [&] {
+        k_clear_isolated_flags<<<grid_for(g.n, kThreads), kThreads, 0, s>>>(wb.flag_a.p, g.cls.p, g.n);
+        CUDA_TRY(cudaGetLastError());
+    });
+    read_counters(ctx);
+    const int64_t ev = (int64_t)(ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI]);
+    const int64_t ar = (int64_t)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI]);
+    ctx->stats.rounds += 1;
+    ctx->stats.vertex_evals += ev;
+    ctx->stats.arc_reads += ar;
+    ctx->stats.first_evals += ev;
+    ctx->stats.first_arcs += ar;
+    return (int64_t)ctx->h_sum[CNT_DELTA];
+}
+
+void slpa_init_labels(slpa_ctx *ctx) {
+    const int64_t n = ctx->g.n;
+    if (n == 0) return;
+    k_init_labels<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(
+        ctx->wb.lab_old.p, ctx->wb.lab_new.p, ctx->wb.flag_a.p, ctx->g.has_order ? ctx->g.ids.p : nullptr, n);
+    CUDA_TRY(cudaGetLastError());
+}
+
+void slpa_labels_to_host(slpa_ctx *ctx, int32_t *host) {
+    const int64_t n = ctx->g.n;
+    if (n == 0) return;
+    const int32_t *src = ctx->wb.lab_old.p;
+    if (ctx->g.has_order) {
+        k_pos_to_id_i32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(src, ctx->wb.io_labels.p, ctx->g.ids.p, n);
+        CUDA_TRY(cudaGetLastError());
+        src = ctx->wb.io_labels.p;
+    }
+    CUDA_TRY(cudaMemcpyAsync(host, src, n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+}
+
+void slpa_labels_from_host(slpa_ctx *ctx, const int32_t *host) {
+    const int64_t n = ctx->g.n;
+    if (n == 0) return;
+    if (ctx->g.has_order) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->wb.io_labels.p, host, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        k_id_to_pos_i32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.io_labels.p, ctx->wb.lab_old.p,
+                                                                              ctx->g.ids.p, n);
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(ctx->wb.lab_old.p, host, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    k_sync_lab_new<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.lab_old.p, ctx->wb.lab_new.p, n);
+    CUDA_TRY(cudaGetLastError());
+}
+
+void slpa_flags_to_host(slpa_ctx *ctx, uint8_t *host) {
+    const int64_t n = ctx->g.n;
+    if (n == 0) return;
+    const uint8_t *src = ctx->wb.flag_a.p;
+    if (ctx->g.has_order) {
+        k_pos_to_id_u8<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(src, ctx->wb.io_flags.p, ctx->g.ids.p, n);
+        CUDA_TRY(cudaGetLastError());
+        src = ctx->wb.io_flags.p;
+    }
+    CUDA_TRY(cudaMemcpyAsync(host, src, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+}
+
+void slpa_flags_from_host(slpa_ctx *ctx, const uint8_t *host) {
+    const int64_t n = ctx->g.n;
+    if (n == 0) return;
+    if (ctx->g.has_order) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->wb.io_flags.p, host, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+        k_id_to_pos_u8<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.io_flags.p, ctx->wb.flag_a.p,
+                                                                             ctx->g.ids.p, n);
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(ctx->wb.flag_a.p, host, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+        k_norm_flags<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.flag_a.p, n);
+    }
+    CUDA_TRY(cudaGetLastError());
+}
+
+void slpa_permute_id_to_pos(slpa_ctx *ctx, const int32_t *d_by_id, int32_t *d_by_pos) {
+    const int64_t n = ctx->g.n;
+    if (n == 0) return;
+    k_id_to_pos_i32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(d_by_id, d_by_pos, ctx->g.ids.p, n);
+    CUDA_TRY(cudaGetLastError());
+}
