@@ -20,7 +20,9 @@ convergence) from fresh labels.
            device time, against MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline: the CPU oracle (C restatement of the reference) on this
            host, 1 thread, a bounded prefix of sweep 0 on the same graph.
-* N > 1  : independent replicas (one full graph per GPU; scaling "weak").
+* N > 1  : one RMAT graph of scale --scale + log2(N) partitioned by contiguous
+           vertex ranges (asynchronous partitioned sweep, NCCL label
+           all-gather + flag max-reduce per sweep); scaling "weak".
 """
 
 from __future__ import annotations
@@ -185,6 +187,67 @@ def workload_config(args, n, m, world):
     }
 
 
+def run_partitioned(args, world, rank, local, dist):
+    """N > 1: one graph partitioned by contiguous vertex ranges, the
+    asynchronous partitioned sweep with an NCCL label all-gather and flag
+    max-reduction per sweep (paper_2411_19901_b200/distributed.py).  Weak
+    scaling: RMAT scale = --scale + log2(N) (N=8: scale 27)."""
+    import math
+    import torch
+    import paper_2411_19901_b200 as slpa
+    from paper_2411_19901_b200.distributed import lpa_run_partitioned, partition_ranges
+    scale = args.scale + int(round(math.log2(world)))
+    n = 1 << scale
+    ranges = partition_ranges(n, world)
+    eng = slpa.Engine(local)
+    eng.part_gen_rmat(scale, *ranges[rank], seed=SEED, permute=True)
+    cfg = slpa.LpaConfig(variant=args.variant, worker_count=1)
+    dev = torch.device(f"cuda:{local}")
+    m_local = torch.tensor([eng.m], dtype=torch.int64, device=dev)
+    dist.all_reduce(m_local)
+    m = int(m_local.item())
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        dist.barrier()
+
+    for _ in range(args.warmup):
+        lpa_run_partitioned(eng, cfg, ranges)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters_all = []
+    ev0.record()
+    for _ in range(args.steps):
+        res = lpa_run_partitioned(eng, cfg, ranges)
+        iters_all.append(res.iterations)
+    ev1.record()
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1) / 1000.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_s = float(t.item())
+    value = float(m) * sum(iters_all) / t_s
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * t_s / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"nuMG8-LPA RMAT s{scale} ef16 partitioned over {world} GPUs",
+                       "graph": f"RMAT scale {scale} (= {args.scale} + log2 N), edge factor 16, permuted, seed {SEED}",
+                       "vertices": n, "arcs": m, "variant": args.variant,
+                       "mode": "async (partitioned; deterministic multi-GPU is not implemented)",
+                       "parallelism": f"{world} contiguous vertex ranges, NCCL label all-gather + flag max-reduce",
+                       "l2_policy": "inputs larger than L2"},
+            "iterations_per_step": iters_all, "gpu_launches": None, "e2e": None, "roofline": None,
+            "cpu_baseline": None, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -213,6 +276,9 @@ def main():
         dist.init_process_group("nccl")
 
     import paper_2411_19901_b200 as slpa
+    if world > 1:
+        run_partitioned(args, world, rank, local, dist)
+        return
     eng = slpa.Engine(local)
     eng.gen_rmat(args.scale, seed=SEED, permute=True)
     n, m = eng.n, eng.m

@@ -75,14 +75,16 @@ typedef struct {
  * it off for throughput runs).  evals / arcs are the vertices evaluated and
  * arcs scanned by those launches -- the algorithmic work. */
 enum {
-    SLPA_PROF_EVAL_LO0 = 0,  /* round-0 low-degree label scan (thread per vertex) */
-    SLPA_PROF_EVAL_HI0 = 1,  /* round-0 high-degree label scan (warp per vertex) */
-    SLPA_PROF_EVAL_LOK = 2,  /* re-evaluation rounds, low degree */
-    SLPA_PROF_EVAL_HIK = 3,  /* re-evaluation rounds, high degree */
-    SLPA_PROF_COMPACT = 4,   /* dirty bitmap -> worklists */
-    SLPA_PROF_COMMIT = 5,    /* label update, flags, changed-vertex count */
-    SLPA_PROF_OTHER = 6,
-    SLPA_PROF_N = 8
+    SLPA_PROF_EVAL_LO0 = 0,  /* round-0 label scan, deg < D_H (lane per vertex) */
+    SLPA_PROF_EVAL_MID0 = 1, /* round-0 label scan, D_H <= deg < split (lane per vertex, R_H chunks) */
+    SLPA_PROF_EVAL_HI0 = 2,  /* round-0 label scan, deg >= split (warp per vertex, lane = chunk) */
+    SLPA_PROF_EVAL_LOK = 3,  /* re-evaluation rounds, same classes */
+    SLPA_PROF_EVAL_MIDK = 4,
+    SLPA_PROF_EVAL_HIK = 5,
+    SLPA_PROF_COMPACT = 6,   /* dirty bitmap -> worklists */
+    SLPA_PROF_COMMIT = 7,    /* label update, flags, changed-vertex count */
+    SLPA_PROF_OTHER = 8,
+    SLPA_PROF_N = 12
 };
 typedef struct {
     int64_t launches[SLPA_PROF_N];
@@ -158,6 +160,32 @@ int64_t slpa_aux_memory_estimate(int64_t n, int32_t value_bytes, const slpa_conf
  * sizes/internal/incident may be NULL. */
 int32_t slpa_modularity(slpa_ctx *ctx, const int32_t *labels, double *q, int64_t *num_communities,
                         int64_t *sizes, double *internal, double *incident);
+
+/* ------------------------------------------------------------ multi-GPU
+ * Contiguous vertex-range partition, one context per rank.
+ * The rank holds the rows of [v_begin, v_end) in the global numbering
+ * (targets are global ids) plus a full label replica.  A partitioned run is
+ * the asynchronous sweep: between sweeps the host all-gathers the owned
+ * label ranges and max-reduces the flag arrays (remote entries carry the
+ * "neighbour changed" marks of lpa.py:223) -- paper_2411_19901_b200/
+ * distributed.py does this with torch.distributed over NCCL. */
+int32_t slpa_part_upload(slpa_ctx *ctx, int64_t n, int64_t v_begin, int64_t v_end, const int64_t *row_offsets,
+                         const int32_t *targets, const void *weights, int32_t weights_f64);
+int32_t slpa_part_gen_rmat(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
+                           uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t v_begin,
+                           int64_t v_end);
+int32_t slpa_part_info(slpa_ctx *ctx, int64_t *n, int64_t *m_local, int64_t *v_begin, int64_t *v_end);
+/* Device pointers of the label replica (int32[n]) and flag array (uint8[n]). */
+int32_t slpa_part_buffers(slpa_ctx *ctx, uint64_t *labels_dptr, uint64_t *flags_dptr);
+int32_t slpa_part_begin(slpa_ctx *ctx, const slpa_config *cfg);
+int32_t slpa_part_sweep(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickless, int64_t *changed_local);
+/* After the exchange: clear the remote (outgoing-mark) flag entries. */
+int32_t slpa_part_end_exchange(slpa_ctx *ctx);
+/* Rank-local tallies: internal weight (scalar) and device float64[n]
+ * incident / int64[n] sizes arrays for an all-reduce; then Q from the
+ * reduced incident array and the summed internal weight. */
+int32_t slpa_part_tally(slpa_ctx *ctx, double *internal_local, uint64_t *incident_dptr, uint64_t *sizes_dptr);
+int32_t slpa_part_modularity(slpa_ctx *ctx, double internal_total, double *q);
 
 #ifdef __cplusplus
 }

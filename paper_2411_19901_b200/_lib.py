@@ -51,8 +51,9 @@ class SlpaRunStats(ctypes.Structure):
     ]
 
 
-PROF_N = 8
-PROF_CLASSES = ("eval_lo_r0", "eval_hi_r0", "eval_lo_rk", "eval_hi_rk", "compact", "commit", "other", "unused")
+PROF_N = 12
+PROF_CLASSES = ("eval_lo_r0", "eval_mid_r0", "eval_hi_r0", "eval_lo_rk", "eval_mid_rk", "eval_hi_rk", "compact",
+                "commit", "other", "unused", "unused", "unused")
 
 
 class SlpaProfile(ctypes.Structure):
@@ -92,6 +93,16 @@ SIGNATURES = {
     "slpa_get_profile": (_i32, [_vp, ctypes.POINTER(SlpaProfile)]),
     "slpa_aux_memory_estimate": (_i64, [_i64, _i32, ctypes.POINTER(SlpaConfig)]),
     "slpa_modularity": (_i32, [_vp, _vp, ctypes.POINTER(_d), ctypes.POINTER(_i64), _vp, _vp, _vp]),
+    "slpa_part_upload": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _i32]),
+    "slpa_part_gen_rmat": (_i32, [_vp, _i32, _i64, _u32, _u32, _u32, _u64, _i32, _u64, _i64, _i64]),
+    "slpa_part_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                              ctypes.POINTER(_i64)]),
+    "slpa_part_buffers": (_i32, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "slpa_part_begin": (_i32, [_vp, ctypes.POINTER(SlpaConfig)]),
+    "slpa_part_sweep": (_i32, [_vp, ctypes.POINTER(SlpaConfig), _i32, ctypes.POINTER(_i64)]),
+    "slpa_part_end_exchange": (_i32, [_vp]),
+    "slpa_part_tally": (_i32, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "slpa_part_modularity": (_i32, [_vp, _d, ctypes.POINTER(_d)]),
 }
 
 _LIB = None

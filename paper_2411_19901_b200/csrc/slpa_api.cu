@@ -79,6 +79,7 @@ void upload_csr(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *off, const i
     g.w_f64 = w_f64 ? 1 : 0;
     slpa_graph_validate(ctx, g.base, g.w_f64);
     ctx->have_labels = 0;
+    ctx->part = 0;
 }
 }  // namespace
 
@@ -105,6 +106,7 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.flag_b.alloc(n);
     wb.dirty_a.alloc(n / 32 + 1);
     wb.wl_lo.alloc(n);
+    wb.wl_mid.alloc(n);
     wb.wl_hi.alloc(n);
     wb.io_labels.alloc(n);
     wb.io_flags.alloc(n);
@@ -165,10 +167,11 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     ctx->g.rsrc.release();
     ctx->g.cls.release();
     ctx->g.bin_lo.release();
+    ctx->g.bin_mid.release();
     ctx->g.bin_hi.release();
     WorkBuffers &wb = ctx->wb;
     wb.lab_old.release(); wb.lab_new.release(); wb.flag_a.release(); wb.flag_b.release();
-    wb.dirty_a.release(); wb.dirty_b.release(); wb.wl_lo.release(); wb.wl_hi.release();
+    wb.dirty_a.release(); wb.dirty_b.release(); wb.wl_lo.release(); wb.wl_mid.release(); wb.wl_hi.release();
     wb.io_labels.release(); wb.io_flags.release(); wb.counters.release(); wb.metric_d.release();
     wb.metric_u.release(); wb.scratch.release();
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -241,6 +244,7 @@ int32_t slpa_graph_download(slpa_ctx *ctx, int64_t *offsets, int32_t *targets, v
 int32_t slpa_gen_rmat(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
                       uint64_t seed, int32_t permute, uint64_t perm_key) {
     return guard(ctx, [&] {
+        ctx->part = 0;
         slpa_gen_rmat_impl(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key);
         slpa_graph_finalize(ctx);
         ctx->have_labels = 0;
@@ -249,6 +253,7 @@ int32_t slpa_gen_rmat(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t 
 
 int32_t slpa_gen_grid(slpa_ctx *ctx, int64_t rows, int64_t cols, int32_t permute, uint64_t perm_key) {
     return guard(ctx, [&] {
+        ctx->part = 0;
         slpa_gen_grid_impl(ctx, rows, cols, permute, perm_key);
         slpa_graph_finalize(ctx);
         ctx->have_labels = 0;
@@ -257,6 +262,7 @@ int32_t slpa_gen_grid(slpa_ctx *ctx, int64_t rows, int64_t cols, int32_t permute
 
 int32_t slpa_gen_kmer(slpa_ctx *ctx, int64_t n, uint32_t keep, uint64_t seed, int32_t permute, uint64_t perm_key) {
     return guard(ctx, [&] {
+        ctx->part = 0;
         slpa_gen_kmer_impl(ctx, n, keep, seed, permute, perm_key);
         slpa_graph_finalize(ctx);
         ctx->have_labels = 0;
@@ -266,6 +272,7 @@ int32_t slpa_gen_kmer(slpa_ctx *ctx, int64_t n, uint32_t keep, uint64_t seed, in
 int32_t slpa_build_graph(slpa_ctx *ctx, int64_t n, int64_t num_edges, const int64_t *src, const int64_t *dst,
                          const double *w, int32_t weights_f64) {
     return guard(ctx, [&] {
+        ctx->part = 0;
         slpa_build_graph_impl(ctx, n, num_edges, src, dst, w, weights_f64);
         slpa_graph_finalize(ctx);
         ctx->have_labels = 0;

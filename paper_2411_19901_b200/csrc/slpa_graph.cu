@@ -3,7 +3,10 @@
 // degree binning (lpa.py:137, :173), and device-side synthetic generators with
 // canonical assembly (graph.py:107-139).  One-time setup work; the sweep
 // kernels are in slpa_sweep.cu.
+#include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 #include <cub/cub.cuh>
 #include "slpa_internal.cuh"
@@ -31,27 +34,42 @@ __global__ void k_validate_arcs(const int32_t *tgt, const W *w, int64_t n, int64
 }
 
 // ------------------------------------------------------------------ symmetry
-// Symmetric (for dependency purposes) iff every row is sorted and every arc
-// u->t has a reverse arc t->u.  One warp per vertex.
-__global__ void k_check_symmetric(const int64_t *off, const int32_t *tgt, int64_t n, unsigned *asym) {
+// The arc multiset is symmetric iff sum_arcs h(u,t) == sum_arcs h(t,u) for a
+// random-looking h; two independent 64-bit mixes make a false "symmetric"
+// verdict a 2^-128 event.  One coalesced pass, one atomic per warp.
+__device__ __forceinline__ uint64_t sym_mix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+__global__ void k_sym_hash(const int64_t *off, const int32_t *tgt, int64_t n, unsigned long long *acc) {
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
+    uint64_t f1 = 0, r1 = 0, f2 = 0, r2 = 0;
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
         const int64_t lo = off[v], hi = off[v + 1];
-        bool bad = false;
         for (int64_t e = lo + lane; e < hi; e += 32) {
-            int32_t t = tgt[e];
-            if (e > lo && tgt[e - 1] > t) bad = true;
-            // binary search v in row t
-            int64_t a = off[t], b = off[t + 1];
-            while (a < b) {
-                int64_t mid = (a + b) >> 1;
-                if (tgt[mid] < v) a = mid + 1;
-                else b = mid;
-            }
-            if (a >= off[t + 1] || tgt[a] != v) bad = true;
+            const uint64_t t = (uint64_t)(uint32_t)tgt[e], u = (uint64_t)v;
+            const uint64_t fw = (u << 32) | t, rv = (t << 32) | u;
+            f1 += sym_mix(fw);
+            r1 += sym_mix(rv);
+            f2 += sym_mix(fw ^ 0x5851F42D4C957F2DULL) * 0x2545F4914F6CDD1DULL;
+            r2 += sym_mix(rv ^ 0x5851F42D4C957F2DULL) * 0x2545F4914F6CDD1DULL;
         }
-        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(asym, 1u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+        f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&acc[0], (unsigned long long)f1);
+        atomicAdd(&acc[1], (unsigned long long)r1);
+        atomicAdd(&acc[2], (unsigned long long)f2);
+        atomicAdd(&acc[3], (unsigned long long)r2);
     }
 }
 
@@ -108,11 +126,12 @@ __global__ void k_perm_rows(const int64_t *off, const int32_t *tgt, const W *w, 
 }
 
 // ------------------------------------------------------------------ bins
-__global__ void k_classify(const int64_t *off, int64_t n, int32_t thr, int32_t single, uint8_t *cls) {
+__global__ void k_classify(const int64_t *off, int64_t n, int32_t thr, int32_t hsplit, int32_t single,
+                           uint8_t *cls) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     int64_t d = off[v + 1] - off[v];
-    cls[v] = d == 0 ? CLS_NONE : ((single || d < thr) ? CLS_LO : CLS_HI);
+    cls[v] = d == 0 ? CLS_NONE : ((single || d < thr) ? CLS_LO : (d < hsplit ? CLS_MID : CLS_HI));
 }
 struct IsClass {
     const uint8_t *cls;
@@ -229,25 +248,31 @@ __global__ void k_gen_kmer(int64_t n, uint32_t keep, uint64_t seed, int32_t perm
 }
 
 // unique pairs (a<=b, count) -> arc keys (src<<32|dst) with weights
-__global__ void k_pair_arity(const uint64_t *pairs, int64_t np, int64_t *arity) {
+// Arcs a->b and b->a of a unique pair, restricted to sources in [r0, r1)
+// (the whole graph, or one rank's rows of a vertex-range partition).
+__global__ void k_pair_arity(const uint64_t *pairs, int64_t np, int64_t *arity, int64_t r0, int64_t r1) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    uint64_t p = pairs[i];
-    arity[i] = ((p >> 32) == (p & 0xFFFFFFFFULL)) ? 1 : 2;
+    const uint64_t p = pairs[i];
+    const int64_t a = (int64_t)(p >> 32), b = (int64_t)(p & 0xFFFFFFFFULL);
+    arity[i] = (a >= r0 && a < r1) + (a != b && b >= r0 && b < r1);
 }
 template <class W>
 __global__ void k_emit_arcs(const uint64_t *pairs, const double *wsum, const int64_t *pos, int64_t np, uint64_t *akeys,
-                            W *aw) {
+                            W *aw, int64_t r0, int64_t r1) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    uint64_t p = pairs[i];
-    uint64_t a = p >> 32, b = p & 0xFFFFFFFFULL;
+    const uint64_t p = pairs[i];
+    const uint64_t a = p >> 32, b = p & 0xFFFFFFFFULL;
     int64_t o = pos[i];
-    akeys[o] = (a << 32) | b;
-    aw[o] = (W)wsum[i];
-    if (a != b) {
-        akeys[o + 1] = (b << 32) | a;
-        aw[o + 1] = (W)wsum[i];
+    if ((int64_t)a >= r0 && (int64_t)a < r1) {
+        akeys[o] = (a << 32) | b;
+        aw[o] = (W)wsum[i];
+        ++o;
+    }
+    if (a != b && (int64_t)b >= r0 && (int64_t)b < r1) {
+        akeys[o] = (b << 32) | a;
+        aw[o] = (W)wsum[i];
     }
 }
 __global__ void k_counts_to_double(const uint32_t *cnt, int64_t np, double *w) {
@@ -368,17 +393,21 @@ void slpa_graph_finalize(slpa_ctx *ctx) {
     cudaStream_t s = ctx->stream;
     g.bin_thr = -1;
     g.bin_single = -1;
+    g.bin_lo_sorted = -1;
     g.roff.release();
     g.rsrc.release();
     g.symmetric = 1;
     if (g.n == 0 || g.m == 0) return;
-    DevBuf<unsigned> flag;
-    flag.alloc(1);
-    CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), s));
-    k_check_symmetric<<<grid_warps(g.n), kT, 0, s>>>(g.off(), g.tgt(), g.n, flag.p);
+    DevBuf<unsigned long long> acc;
+    acc.alloc(4);
+    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 4 * sizeof(unsigned long long), s));
+    k_sym_hash<<<grid_warps(g.n), kT, 0, s>>>(g.off(), g.tgt(), g.n, acc.p);
     CUDA_TRY(cudaGetLastError());
-    g.symmetric = read_flag(ctx, flag.p) == 0;
-    flag.release();
+    unsigned long long h[4];
+    CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    acc.release();
+    g.symmetric = (h[0] == h[1]) && (h[2] == h[3]);
     if (g.symmetric) return;
     // reverse CSR: in-degree histogram, exclusive scan, atomic fill
     g.roff.alloc(g.n + 1);
@@ -465,6 +494,14 @@ void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order, bool on_device)
     slpa_graph_finalize(ctx);
 }
 
+static int64_t hi_split() {
+    static int64_t v = [] {
+        const char *e = getenv("SLPA_HI_SPLIT");
+        return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)1;
+    }();
+    return v;
+}
+
 // Degree bins for a threshold (lpa.py:137, :173): low = 0 < deg < thr
 // (ascending position), high = deg >= thr (descending degree, so the longest
 // scans start first).  `single` puts every non-empty vertex in the low bin.
@@ -472,47 +509,75 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
     DeviceGraph &g = ctx->g;
     cudaStream_t s = ctx->stream;
     const int single = (cfg->variant == SLPA_VARIANT_EXACT) || (cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch);
-    if (g.bin_thr == cfg->degree_threshold && g.bin_single == single) return;
+    // deterministic mode: degree-sorted low bin (homogeneous warps); async
+    // mode: ascending positions (closest to the sequential visiting order,
+    // which async quality depends on)
+    static const int lo_sort_env = [] {
+        const char *e = getenv("SLPA_LO_SORT");
+        return e ? atoi(e) : -1;
+    }();
+    const int lo_sorted = lo_sort_env >= 0 ? lo_sort_env : (cfg->worker_count == 0);
+    if (g.bin_thr == cfg->degree_threshold && g.bin_single == single && g.bin_lo_sorted == lo_sorted) return;
     const int64_t n = g.n;
     g.cls.alloc(n);
     g.bin_lo.alloc(n);
+    g.bin_mid.alloc(n);
     g.bin_hi.alloc(n);
-    if (n > 0) k_classify<<<grid_for(n, kT), kT, 0, s>>>(g.off(), n, cfg->degree_threshold, single, g.cls.p);
+    // Bins are an execution split: lo = deg < D_H (one lane, one sketch),
+    // mid = D_H <= deg < max(D_H, hi_split) (one lane, R_H chunks),
+    // hi = the rest (one warp, lane = chunk).
+    const int64_t hs = std::max<int64_t>(cfg->degree_threshold, hi_split());
+    const int32_t hsplit = (int32_t)std::min<int64_t>(hs, INT32_MAX);
+    if (n > 0) k_classify<<<grid_for(n, kT), kT, 0, s>>>(g.off(), n, cfg->degree_threshold, hsplit, single, g.cls.p);
     CUDA_TRY(cudaGetLastError());
     DevBuf<int64_t> cnt;
-    cnt.alloc(2);
+    cnt.alloc(3);
     cub::CountingInputIterator<int32_t> it(0);
-    for (int which = 0; which < 2; ++which) {
-        IsClass pred{g.cls.p, (uint8_t)(which == 0 ? CLS_LO : CLS_HI)};
-        int32_t *out = which == 0 ? g.bin_lo.p : g.bin_hi.p;
+    const uint8_t classes[3] = {CLS_LO, CLS_MID, CLS_HI};
+    int32_t *outs[3] = {g.bin_lo.p, g.bin_mid.p, g.bin_hi.p};
+    for (int which = 0; which < 3; ++which) {
+        IsClass pred{g.cls.p, classes[which]};
+        int32_t *out = outs[which];
         int64_t *nsel = cnt.p + which;
         cub_call(ctx, [&](void *tmp, size_t &bytes) {
             return cub::DeviceSelect::If(tmp, bytes, it, out, nsel, n, pred, s);
         });
     }
-    int64_t h[2] = {0, 0};
+    int64_t h[3] = {0, 0, 0};
     CUDA_TRY(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     g.n_lo = h[0];
-    g.n_hi = h[1];
-    if (g.n_hi > 1) {  // descending degree
+    g.n_mid = h[1];
+    g.n_hi = h[2];
+    // hi: descending degree (longest scans first); lo / mid: ascending
+    // degree, stable on position (degree-homogeneous warps)
+    for (int which = 0; which < 3; ++which) {
+        const int64_t cntb = which == 2 ? g.n_hi : (which == 1 ? g.n_mid : (lo_sorted ? g.n_lo : 0));
+        int32_t *binp = outs[which];
+        if (cntb <= 1) continue;
         DevBuf<int64_t> dk, dk2;
         DevBuf<int32_t> v2;
-        dk.alloc(g.n_hi);
-        dk2.alloc(g.n_hi);
-        v2.alloc(g.n_hi);
-        k_bin_degrees<<<grid_for(g.n_hi, kT), kT, 0, s>>>(g.off(), g.bin_hi.p, g.n_hi, dk.p);
+        dk.alloc(cntb);
+        dk2.alloc(cntb);
+        v2.alloc(cntb);
+        k_bin_degrees<<<grid_for(cntb, kT), kT, 0, s>>>(g.off(), binp, cntb, dk.p);
         int64_t *k1 = dk.p, *k2 = dk2.p;
-        int32_t *v1 = g.bin_hi.p, *vv2 = v2.p;
-        int64_t nh = g.n_hi;
-        cub_call(ctx, [&](void *tmp, size_t &bytes) {
-            return cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k1, k2, v1, vv2, nh, 0, 64, s);
-        });
-        CUDA_TRY(cudaMemcpyAsync(g.bin_hi.p, v2.p, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        int32_t *v1 = binp, *vv2 = v2.p;
+        const int64_t nh = cntb;
+        if (which == 2)
+            cub_call(ctx, [&](void *tmp, size_t &bytes) {
+                return cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k1, k2, v1, vv2, nh, 0, 40, s);
+            });
+        else
+            cub_call(ctx, [&](void *tmp, size_t &bytes) {
+                return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, v1, vv2, nh, 0, 40, s);
+            });
+        CUDA_TRY(cudaMemcpyAsync(binp, v2.p, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(cudaStreamSynchronize(s));
     }
     g.bin_thr = cfg->degree_threshold;
     g.bin_single = single;
+    g.bin_lo_sorted = lo_sorted;
 }
 
 // Unique canonical pairs (a<=b, sorted) + merged float64 weights -> CSR:
@@ -520,14 +585,14 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
 // (src, dst) (graph.py:135-136), offsets by binary search, cast weights.
 template <class W>
 static void assemble_pairs_t(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &pairs, int64_t np, DevBuf<double> &wsum,
-                             int end_bit, DevBuf<W> &out_w) {
+                             int end_bit, DevBuf<W> &out_w, int64_t r0, int64_t r1) {
     cudaStream_t s = ctx->stream;
     DeviceGraph &g = ctx->g;
     DevBuf<int64_t> arity, posn;
     arity.alloc(np + 1);
     posn.alloc(np + 1);
     CUDA_TRY(cudaMemsetAsync(arity.p, 0, (np + 1) * sizeof(int64_t), s));
-    if (np > 0) k_pair_arity<<<grid_for(np, kT), kT, 0, s>>>(pairs.p, np, arity.p);
+    if (np > 0) k_pair_arity<<<grid_for(np, kT), kT, 0, s>>>(pairs.p, np, arity.p, r0, r1);
     {
         int64_t *ain = arity.p, *aout = posn.p;
         int64_t nn = np + 1;
@@ -541,7 +606,7 @@ static void assemble_pairs_t(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &pairs, 
     DevBuf<W> aw;
     akeys.alloc(m);
     aw.alloc(m);
-    if (np > 0) k_emit_arcs<W><<<grid_for(np, kT), kT, 0, s>>>(pairs.p, wsum.p, posn.p, np, akeys.p, aw.p);
+    if (np > 0) k_emit_arcs<W><<<grid_for(np, kT), kT, 0, s>>>(pairs.p, wsum.p, posn.p, np, akeys.p, aw.p, r0, r1);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));
     pairs.release();
@@ -577,16 +642,18 @@ static void assemble_pairs_t(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &pairs, 
 }
 
 static void assemble_pairs(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &pairs, int64_t np, DevBuf<double> &wsum,
-                           int end_bit, int w_f64) {
+                           int end_bit, int w_f64, int64_t r0 = 0, int64_t r1 = -1) {
     ctx->g.base.release();
     ctx->g.w_f64 = w_f64 ? 1 : 0;
-    if (w_f64) assemble_pairs_t<double>(ctx, n, pairs, np, wsum, end_bit, ctx->g.base.w64);
-    else assemble_pairs_t<float>(ctx, n, pairs, np, wsum, end_bit, ctx->g.base.w32);
+    if (r1 < 0) r1 = n;
+    if (w_f64) assemble_pairs_t<double>(ctx, n, pairs, np, wsum, end_bit, ctx->g.base.w64, r0, r1);
+    else assemble_pairs_t<float>(ctx, n, pairs, np, wsum, end_bit, ctx->g.base.w32, r0, r1);
 }
 
 // Unit-weight edge keys (min<<32|max, `drop` = removed): sort, run-length
 // encode (duplicate count = merged weight, exact in any order), assemble.
-static void assemble_from_keys(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &keys, int64_t ne, int end_bit) {
+static void assemble_from_keys(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &keys, int64_t ne, int end_bit,
+                               int64_t r0 = 0, int64_t r1 = -1) {
     cudaStream_t s = ctx->stream;
     DevBuf<uint64_t> sorted;
     sorted.alloc(ne);
@@ -624,7 +691,7 @@ static void assemble_from_keys(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &keys,
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));
     counts.release();
-    assemble_pairs(ctx, n, keys, np, wsum, end_bit, 0);
+    assemble_pairs(ctx, n, keys, np, wsum, end_bit, 0, r0, r1);
 }
 
 static int key_end_bit(int64_t n) { return 32 + ceil_log2((uint64_t)(n > 1 ? n : 2)) + 1; }
@@ -745,4 +812,69 @@ void slpa_build_graph_impl(slpa_ctx *ctx, int64_t n, int64_t ne, const int64_t *
     counts.release();
     starts.release();
     assemble_pairs(ctx, n, keys, np, wsum, end_bit, weights_f64);
+}
+
+// ---------------------------------------------------------------- partition
+namespace {
+struct TouchesRange {
+    int64_t r0, r1;
+    __host__ __device__ bool operator()(const uint64_t &k) const {
+        const int64_t a = (int64_t)(k >> 32), b = (int64_t)(k & 0xFFFFFFFFULL);
+        return (a >= r0 && a < r1) || (b >= r0 && b < r1);
+    }
+};
+}  // namespace
+
+// One rank's rows of the RMAT graph: every rank generates the
+// same edge stream (counter-based RNG) in chunks, keeps the pairs touching
+// its vertex range, and assembles only arcs whose source it owns.  Offsets
+// stay global (n+1, rows outside the range empty), targets are global ids.
+void slpa_part_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
+                             uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t r0,
+                             int64_t r1) {
+    SLPA_REQUIRE(scale >= 1 && scale <= 31, SLPA_EINVAL, "rmat scale must be in [1, 31]");
+    const int64_t n = 1LL << scale;
+    SLPA_REQUIRE(r0 >= 0 && r0 <= r1 && r1 <= n, SLPA_EINVAL, "bad vertex range");
+    cudaStream_t s = ctx->stream;
+    const int64_t chunk = std::min<int64_t>(num_edges, 1LL << 27);
+    DevBuf<uint64_t> buf, kept, sel;
+    DevBuf<int64_t> nsel;
+    buf.alloc(chunk);
+    nsel.alloc(1);
+    std::vector<DevBuf<uint64_t>> parts;
+    int64_t total = 0;
+    std::vector<int64_t> sizes;
+    for (int64_t e0 = 0; e0 < num_edges; e0 += chunk) {
+        const int64_t cnt = std::min(chunk, num_edges - e0);
+        k_gen_rmat<<<grid_for(cnt, kT), kT, 0, s>>>(scale, e0, cnt, tA, tAB, tABC, seed, permute, perm_key,
+                                                    drop_key(n), buf.p);
+        CUDA_TRY(cudaGetLastError());
+        DevBuf<uint64_t> out;
+        out.alloc(cnt);
+        uint64_t *in = buf.p, *o = out.p;
+        int64_t *ns = nsel.p;
+        TouchesRange pred{r0, r1};
+        cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceSelect::If(tmp, bytes, in, o, ns, cnt, pred, s); });
+        int64_t h = 0;
+        CUDA_TRY(cudaMemcpyAsync(&h, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        parts.push_back(DevBuf<uint64_t>());
+        parts.back().p = out.p;
+        parts.back().count = out.count;
+        out.p = nullptr;
+        out.count = 0;
+        sizes.push_back(h);
+        total += h;
+    }
+    buf.release();
+    kept.alloc(total + 1);
+    int64_t off = 0;
+    for (size_t i = 0; i < parts.size(); ++i) {
+        if (sizes[i]) CUDA_TRY(cudaMemcpyAsync(kept.p + off, parts[i].p, sizes[i] * sizeof(uint64_t),
+                                               cudaMemcpyDeviceToDevice, s));
+        off += sizes[i];
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (auto &p : parts) p.release();
+    assemble_from_keys(ctx, n, kept, total, key_end_bit(n), r0, r1);
 }

@@ -23,7 +23,7 @@
 #define SLPA_KDYN 64          // max sketch slots on the dynamic-k path
 #define SLPA_KHI_MAX 32       // slot-parallel merge holds one slot per lane
 
-enum { CLS_NONE = 0, CLS_LO = 1, CLS_HI = 2 };
+enum { CLS_NONE = 0, CLS_LO = 1, CLS_HI = 2, CLS_MID = 3 };
 
 struct SlpaError {
     int32_t code;
@@ -80,9 +80,11 @@ struct SweepArgs {
     int32_t parts;                    // partial_groups
     int32_t scan_double;
     int32_t symmetric;
+    int32_t thr;                      // degree_threshold (chunked evaluation at deg >= thr)
+    int32_t single;                   // shared_sketch: one sketch over any degree
 };
 
-enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_N = 8 };
+enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_N = 8 };
 #define CNT_STRIPES 64
 #define CNT_TOTAL (CNT_N * CNT_STRIPES)
 
@@ -110,16 +112,17 @@ struct DeviceGraph {
     // degree bins (per threshold)
     int32_t bin_thr = -1;
     int32_t bin_single = -1;  // all non-empty vertices in the low bin (exact / shared sketch)
+    int32_t bin_lo_sorted = -1;
     DevBuf<uint8_t> cls;
-    DevBuf<int32_t> bin_lo, bin_hi;
-    int64_t n_lo = 0, n_hi = 0;
+    DevBuf<int32_t> bin_lo, bin_mid, bin_hi;
+    int64_t n_lo = 0, n_mid = 0, n_hi = 0;
     const Csr &act() const { return has_order ? perm : base; }
     const int64_t *off() const { return act().off.p; }
     const int32_t *tgt() const { return act().tgt.p; }
     const void *w() const { return w_f64 ? (const void *)act().w64.p : (const void *)act().w32.p; }
     size_t bytes() const {
         return base.bytes() + perm.bytes() + ids.bytes() + pos.bytes() + roff.bytes() + rsrc.bytes() + cls.bytes() +
-               bin_lo.bytes() + bin_hi.bytes();
+               bin_lo.bytes() + bin_mid.bytes() + bin_hi.bytes();
     }
     size_t csr_bytes() const { return act().bytes(); }
 };
@@ -129,7 +132,7 @@ struct WorkBuffers {
     DevBuf<uint32_t> lab_new;
     DevBuf<uint8_t> flag_a, flag_b;
     DevBuf<uint32_t> dirty_a, dirty_b;
-    DevBuf<int32_t> wl_lo, wl_hi;
+    DevBuf<int32_t> wl_lo, wl_mid, wl_hi;
     DevBuf<int32_t> io_labels;  // staging for host <-> device label exchange
     DevBuf<uint8_t> io_flags;
     DevBuf<unsigned long long> counters;
@@ -138,7 +141,7 @@ struct WorkBuffers {
     DevBuf<unsigned char> scratch;  // cub temp storage
     size_t bytes() const {
         return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() +
-               dirty_b.bytes() + wl_lo.bytes() + wl_hi.bytes() + io_labels.bytes() + io_flags.bytes() +
+               dirty_b.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
     }
 };

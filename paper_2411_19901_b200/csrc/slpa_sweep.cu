@@ -29,16 +29,42 @@ constexpr int kThreads = 256;
 // ------------------------------------------------------------------ label reads
 // Deterministic mode: neighbour t of v (positions).  Lower neighbours give
 // L1 (speculative, possibly written this round -> L2 load), higher ones L0.
+// The hot array is lab_new (L1 | changed<<31); a higher neighbour's L0 is
+// fetched from lab_old only when its changed bit is set, so most gathers
+// touch one n*4-byte array (L2-resident at RMAT scale 24).
 __device__ __forceinline__ int32_t det_label(const SweepArgs &a, int32_t t, int32_t v, bool &lower_changed) {
+    const uint32_t L = __ldcg(&a.lab_new[t]);
     if (t < v) {
-        uint32_t L = __ldcg(&a.lab_new[t]);
         lower_changed |= (L >> 31) != 0;
         return (int32_t)(L & SLPA_LMASK);
     }
-    return __ldg(&a.lab_old[t]);
+    return (L >> 31) ? __ldg(&a.lab_old[t]) : (int32_t)L;
 }
 
 __device__ __forceinline__ int32_t async_label(const SweepArgs &a, int32_t t) { return __ldcg(&a.lab_old[t]); }
+
+// CSR streams (read once per sweep) are loaded with an L2 evict-first policy
+// so they do not push the label array out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *ptr, uint64_t pol) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float ld_stream(const float *ptr, uint64_t pol) {
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_stream(const double *ptr, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
 
 template <class W>
 __device__ __forceinline__ double arc_weight(const SweepArgs &a, int64_t e) {
@@ -154,17 +180,264 @@ __device__ __forceinline__ void warp_hi_finish(const SweepArgs &a, int32_t v, in
     }
 }
 
-// ================================================================== MG, low degree
-// One thread per vertex, one register-resident k-slot sketch over the
-// non-self arcs in adjacency order (lpa.py:173-177), optional rescan
-// (lpa.py:187-191), max_key or the current label (lpa.py:192-193).
-// No early returns: every lane reaches the warp-aggregated counters.
-template <class W, int K, bool DET>
-__global__ void __launch_bounds__(kThreads) k_mg_lo(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
-                                                    int round0) {
+// ================================================================== window staging
+// A warp runs 32 sequential streams (one per lane): 32 rows (low degree) or
+// the 32 chunks of one vertex (high degree).  For each window of S steps the
+// warp stages the next <= S arcs of every stream into a padded shared tile
+// [lane][step] -- the concatenated window is loaded with consecutive lanes on
+// consecutive arcs (coalesced targets / weights, 32 independent label
+// gathers per instruction) -- then every lane replays its own S steps in
+// order.  Self-arcs are staged with weight 0 (weights are > 0).
+constexpr int kWinWarps = 4;
+constexpr int kWinThreads = kWinWarps * 32;
+
+template <class W>
+struct WinS {
+    static constexpr int S = sizeof(W) == 4 ? 32 : 16;
+};
+
+template <class W, bool DET, bool GRID, class Consume>
+__device__ __forceinline__ void window_streams(const SweepArgs &a, uint32_t (*s_lab)[WinS<W>::S + 1],
+                                               W (*s_w)[WinS<W>::S + 1], int lane, int64_t start, int64_t len,
+                                               int32_t sv, bool &lower_changed, Consume &&consume) {
+    constexpr int S = WinS<W>::S;
+    constexpr int G = 8;  // staging iterations in flight per lane
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    const uint64_t pol = policy_evict_first();
+    int64_t maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int64_t x = __shfl_xor_sync(0xffffffffu, maxlen, o);
+        maxlen = x > maxlen ? x : maxlen;
+    }
+    for (int64_t s0 = 0; s0 < maxlen; s0 += S) {
+        const int64_t rem = len - s0;
+        const int seg = rem <= 0 ? 0 : (rem >= S ? S : (int)rem);
+        int excl = 0, total = 0, iters;
+        if (GRID) {
+            // stream j's window is staged by iteration j, lane = step (coalesced)
+            iters = 32;
+        } else {
+            int incl = seg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int x = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += x;
+            }
+            excl = incl - seg;
+            total = __shfl_sync(0xffffffffu, incl, 31);
+            iters = (total + 31) >> 5;
+        }
+        for (int j0 = 0; j0 < iters; j0 += G) {
+            int32_t t[G], ov[G];
+            W w[G];
+            int own[G], stp[G];
+            bool ok[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const int j = j0 + u;
+                int o, sp;
+                bool valid;
+                if (GRID) {
+                    o = j & 31;
+                    sp = lane;
+                    const int sj = __shfl_sync(0xffffffffu, seg, o);
+                    valid = j < 32 && lane < sj;
+                } else {
+                    const int va = j * 32 + lane;
+                    o = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        int ex = __shfl_sync(0xffffffffu, excl, (o + step) & 31);
+                        if (o + step < 32 && ex <= va) o += step;
+                    }
+                    sp = va - __shfl_sync(0xffffffffu, excl, o);
+                    valid = va < total;
+                }
+                const int64_t o_start = __shfl_sync(0xffffffffu, start, o);
+                ov[u] = __shfl_sync(0xffffffffu, sv, o);
+                own[u] = o;
+                stp[u] = sp;
+                ok[u] = valid;
+                if (valid) {
+                    const int64_t e = o_start + s0 + sp;
+                    t[u] = ld_stream(&a.tgt[e], pol);
+                    w[u] = ld_stream(&wts[e], pol);
+                } else {
+                    t[u] = 0;
+                    w[u] = (W)0;
+                }
+            }
+            uint32_t L[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                L[u] = 0;
+                if (ok[u] && t[u] != ov[u]) L[u] = DET ? __ldcg(&a.lab_new[t[u]]) : (uint32_t)__ldcg(&a.lab_old[t[u]]);
+            }
+            if (DET) {  // higher neighbour that changed this sweep: its L0
+#pragma unroll
+                for (int u = 0; u < G; ++u)
+                    if (ok[u] && t[u] > ov[u] && (L[u] >> 31)) L[u] = (uint32_t)__ldg(&a.lab_old[t[u]]);
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                if (ok[u]) {
+                    s_lab[own[u]][stp[u]] = L[u];
+                    s_w[own[u]][stp[u]] = (t[u] == ov[u]) ? (W)0 : w[u];
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll 4
+        for (int x = 0; x < seg; ++x) {
+            const W w = s_w[lane][x];
+            const uint32_t L = s_lab[lane][x];
+            const bool valid = w != (W)0;
+            lower_changed |= valid && (L >> 31) != 0;
+            consume(s0 + x, valid, (int32_t)(L & SLPA_LMASK), (double)w);
+        }
+        __syncwarp();
+    }
+}
+
+// ================================================================== lane kernels
+// One lane per vertex.  Lane outputs are written per lane; adjacency walks
+// for changed vertices (dependant marks in deterministic mode, neighbour
+// flags in async mode) are done by the whole warp, one changed lane at a
+// time, so they are coalesced instead of 32 divergent row loops.
+template <bool DET>
+__device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t v, int32_t cur, int32_t cand,
+                                            bool T, int64_t lo, int64_t deg, unsigned long long &n_delta) {
+    const int lane = threadIdx.x & 31;
+    bool walk = false;
+    if (go) {
+        if (DET) {
+            const bool chg = T && cand != cur && (!a.pickless || cand < cur);
+            const uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
+            if (nw != __ldcg(&a.lab_new[v])) {
+                __stcg(&a.lab_new[v], nw);
+                walk = true;
+            }
+        } else if (cand != cur && (!a.pickless || cand < cur)) {
+            __stcg(&a.lab_old[v], cand);
+            n_delta = 1;
+            walk = true;
+        }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, walk);
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t vj = __shfl_sync(0xffffffffu, v, j);
+        const int64_t lj = __shfl_sync(0xffffffffu, lo, j);
+        const int64_t hj = lj + __shfl_sync(0xffffffffu, deg, j);
+        if (DET) mark_dependants(a, vj, lj, hj, lane, 32);
+        else
+            for (int64_t e = lj + lane; e < hj; e += 32) a.flag_cur[__ldg(&a.tgt[e])] = 1;
+    }
+}
+
+// MG over one row.  CHUNKED: the R_H chunks of _chunk_bounds (lpa.py:110-118)
+// are cut by arc position while the row streams; each finished chunk is
+// folded into parts[0] right away -- the same replay sequence as
+// sk = parts[0]; sk.merge(parts[1]); ... (lpa.py:179-186, sketch.py:76-91).
+template <int K, bool CHUNKED>
+struct MgLane {
+    static constexpr bool kHasRescan = true;
+    MgSketchDev<K> S, part;
+    int k, p;
+    int64_t base, rem, next;
+    __device__ __forceinline__ void init(int k_, int32_t, int64_t deg, int P) {
+        k = K > 0 ? K : k_;
+        S.reset(k);
+        if (CHUNKED) {
+            part.reset(k);
+            p = 0;
+            base = deg / P;
+            rem = deg % P;
+            next = base + (rem > 0 ? 1 : 0);
+        }
+    }
+    __device__ __forceinline__ void end_chunk() {
+        if (p == 0) {
+            S = part;
+        } else {
+#pragma unroll
+            for (int i = 0; i < KArr<K>::v; ++i) {
+                if (K == 0 && i >= k) break;
+                if (part.val[i] > 0.0) S.acc(part.key[i], part.val[i], k);
+            }
+        }
+        part.reset(k);
+        ++p;
+        next += base + (p < rem ? 1 : 0);
+    }
+    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, double w) {
+        if (CHUNKED) {
+            if (pos == next) end_chunk();
+            if (valid) part.acc(c, w, k);
+        } else if (valid) {
+            S.acc(c, w, k);
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (CHUNKED) end_chunk();
+    }
+    __device__ __forceinline__ void rescan_begin() { S.clear_values(k); }
+    __device__ __forceinline__ void rescan(int32_t c, double w) { S.rescan_add(c, w, k); }
+    __device__ __forceinline__ int32_t result(int32_t cur) const {
+        int32_t b;
+        return S.max_key(k, b) ? b : cur;  // lpa.py:192-193
+    }
+};
+
+// BM over one row: one BmState(cur, 0) per chunk, reduce_votes pair-max
+// (lpa.py:137-150); unchunked rows are a single vote.
+template <bool CHUNKED>
+struct BmLane {
+    static constexpr bool kHasRescan = false;
+    BmVote st, best;
+    int32_t cur0;
+    int p;
+    int64_t base, rem, next;
+    __device__ __forceinline__ void init(int, int32_t cur, int64_t deg, int P) {
+        cur0 = cur;
+        st = BmVote{cur, 0.0};
+        if (CHUNKED) {
+            p = 0;
+            base = deg / P;
+            rem = deg % P;
+            next = base + (rem > 0 ? 1 : 0);
+        }
+    }
+    __device__ __forceinline__ void end_chunk() {
+        if (p == 0 || bm_better(st.w, st.cand, best.w, best.cand)) best = st;
+        st = BmVote{cur0, 0.0};
+        ++p;
+        next += base + (p < rem ? 1 : 0);
+    }
+    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, double w) {
+        if (CHUNKED && pos == next) end_chunk();
+        if (valid) st.acc(c, w);
+    }
+    __device__ __forceinline__ void finish() {
+        if (CHUNKED) end_chunk();
+        else best = st;
+    }
+    __device__ __forceinline__ void rescan_begin() {}
+    __device__ __forceinline__ void rescan(int32_t, double) {}
+    __device__ __forceinline__ int32_t result(int32_t) const { return best.cand; }
+};
+
+template <class W, class Pol, bool DET>
+__global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int32_t *__restrict__ list,
+                                                          int64_t count, int round0) {
+    constexpr int S = WinS<W>::S;
+    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
+    __shared__ W s_w[kWinWarps][32][S + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
-    int32_t v = 0;
+    int32_t v = -1;
     uint8_t f0 = 0;
     bool go = false;
     if (i < count) {
@@ -172,54 +445,47 @@ __global__ void __launch_bounds__(kThreads) k_mg_lo(SweepArgs a, const int32_t *
         f0 = a.flag_cur[v];
         go = DET ? (!round0 || f0) : (f0 != 0);
     }
+    int64_t lo = 0, deg = 0;
+    int32_t cur = 0;
     if (go) {
         if (!DET) a.flag_cur[v] = 0;
-        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-        const int k = K > 0 ? K : a.k;
-        bool lower_changed = false;
-        MgSketchDev<K> sk;
-        sk.reset(k);
-        for (int64_t e = lo; e < hi; ++e) {
-            int32_t t = __ldg(&a.tgt[e]);
-            if (t == v) continue;
-            int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
-            sk.acc(c, arc_weight<W>(a, e), k);
-        }
-        if (a.scan_double) {
-            sk.clear_values(k);
-            bool dummy = false;
-            for (int64_t e = lo; e < hi; ++e) {
-                int32_t t = __ldg(&a.tgt[e]);
-                if (t == v) continue;
-                int32_t c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
-                sk.rescan_add(c, arc_weight<W>(a, e), k);
-            }
-        }
-        int32_t best;
-        const int32_t cand = sk.max_key(k, best) ? best : cur;
-        n_eval = 1;
-        n_arcs = (unsigned long long)(hi - lo);
-        if (DET) {
-            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
-            det_commit_output(a, v, cur, cand, T, lo, hi);
-        } else {
-            async_commit_output(a, v, cur, cand, lo, hi, n_delta);
-        }
+        lo = __ldg(&a.off[v]);
+        deg = __ldg(&a.off[v + 1]) - lo;
+        cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     }
-    warp_count(a.counters, n_eval, n_arcs, n_delta);
+    Pol pol;
+    pol.init(a.k, cur, deg, a.parts);
+    bool lower_changed = false;
+    window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, lower_changed,
+                                  [&](int64_t pos, bool valid, int32_t c, double w) { pol.on(pos, valid, c, w); });
+    if (go && deg) pol.finish();
+    if (Pol::kHasRescan && a.scan_double) {
+        pol.rescan_begin();
+        bool dummy = false;
+        window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, dummy,
+                                      [&](int64_t, bool valid, int32_t c, double w) {
+                                          if (valid) pol.rescan(c, w);
+                                      });
+    }
+    unsigned long long n_delta = 0;
+    const int32_t cand = (go && deg) ? pol.result(cur) : cur;
+    const bool T = go && (f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v)));
+    lane_finish<DET>(a, go, v, cur, cand, T, lo, deg, n_delta);
+    warp_count(a.counters, go ? 1ull : 0ull, (unsigned long long)deg, n_delta);
 }
 
-// ================================================================== MG, high degree
-// One warp per vertex.  Lane g owns chunk g of _chunk_bounds(deg, R_H)
-// (lpa.py:178-183) and a register sketch; parts are then merged into
-// parts[0] in order, replaying each part's non-empty slots ascending
-// (sketch.py:76-91), on a slot-parallel warp sketch (lane l = slot l).
+// High degree, MG: warp per vertex, lane g = chunk g of _chunk_bounds(deg,
+// R_H) (lpa.py:178-183) with a register sketch, streamed through the window
+// tile; then parts[1..] are replayed into parts[0] in order (sketch.py:
+// 76-91) on a slot-parallel warp sketch (lane l = slot l).
 template <class W, int K, bool DET>
-__global__ void __launch_bounds__(kThreads) k_mg_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
-                                                    int round0) {
+__global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int round0) {
+    constexpr int S = WinS<W>::S;
+    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
+    __shared__ W s_w[kWinWarps][32][S + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
     if (wid >= count) return;  // warp-uniform
     const int32_t v = __ldg(&list[wid]);
     const uint8_t f0 = a.flag_cur[v];
@@ -236,21 +502,17 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi(SweepArgs a, const int32_t *
     const int k = K > 0 ? K : a.k;
     const int P = a.parts;
     bool lower_changed = false;
-    WarpSketch S{0, 0.0};
+    WarpSketch S_{0, 0.0};
     for (int b0 = 0; b0 < P; b0 += 32) {
         const int p = b0 + lane;
         MgSketchDev<K> part;
         part.reset(k);
-        if (p < P) {
-            int64_t s, e;
-            chunk_bounds(deg, P, p, s, e);
-            for (int64_t x = lo + s; x < lo + e; ++x) {
-                int32_t t = __ldg(&a.tgt[x]);
-                if (t == v) continue;
-                int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
-                part.acc(c, arc_weight<W>(a, x), k);
-            }
-        }
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
+        window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
+                               [&](int64_t, bool valid, int32_t c, double w) {
+                                         if (valid) part.acc(c, w, k);
+                                     });
         int first = 0;
         if (b0 == 0) {  // sk = parts[0]
 #pragma unroll
@@ -258,23 +520,32 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi(SweepArgs a, const int32_t *
                 if (K == 0 && i >= k) break;
                 int32_t kk = __shfl_sync(0xffffffffu, part.key[i], 0);
                 double vv = __shfl_sync(0xffffffffu, part.val[i], 0);
-                if (lane == i) { S.key = kk; S.val = vv; }
+                if (lane == i) { S_.key = kk; S_.val = vv; }
             }
             first = 1;
         }
         const int nb = min(32, P - b0);
+        unsigned nz = 0;
+#pragma unroll
+        for (int i = 0; i < KArr<K>::v; ++i) {
+            if (K == 0 && i >= k) break;
+            if (part.val[i] > 0.0) nz |= 1u << (i & 31);
+        }
         for (int q = first; q < nb; ++q) {
+            const unsigned mq = __shfl_sync(0xffffffffu, nz, q);
+            if (!mq) continue;
 #pragma unroll
             for (int i = 0; i < KArr<K>::v; ++i) {
                 if (K == 0 && i >= k) break;
+                if (!(mq & (1u << (i & 31)))) continue;
                 int32_t c = __shfl_sync(0xffffffffu, part.key[i], q);
                 double w = __shfl_sync(0xffffffffu, part.val[i], q);
-                if (w > 0.0) S.acc(lane, k, c, w);
+                S_.acc(lane, k, c, w);
             }
         }
     }
     if (a.scan_double) {  // exact per-key re-count in adjacency order
-        S.val = 0.0;
+        S_.val = 0.0;
         bool dummy = false;
         for (int64_t base = lo; base < hi; base += 32) {
             int64_t x = base + lane;
@@ -295,63 +566,24 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi(SweepArgs a, const int32_t *
                 okm &= okm - 1;
                 int32_t cj = __shfl_sync(0xffffffffu, c, j);
                 double wj = __shfl_sync(0xffffffffu, w, j);
-                S.rescan_add(lane, k, cj, wj);
+                S_.rescan_add(lane, k, cj, wj);
             }
         }
     }
     int32_t best;
-    const bool found = S.max_key(lane, k, best);
-    const int32_t cand = found ? best : cur;
-    warp_hi_finish<DET>(a, v, cur, cand, f0, lower_changed, lo, hi, lane);
+    const bool found = S_.max_key(lane, k, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
 }
 
-// ================================================================== BM
-// Low degree: one BmState(cur, 0.0) over the non-self arcs (lpa.py:137-142).
+// High degree, BM: one vote per chunk, pair-max reduce (lpa.py:143-150).
 template <class W, bool DET>
-__global__ void __launch_bounds__(kThreads) k_bm_lo(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
-                                                    int round0) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
-    int32_t v = 0;
-    uint8_t f0 = 0;
-    bool go = false;
-    if (i < count) {
-        v = __ldg(&list[i]);
-        f0 = a.flag_cur[v];
-        go = DET ? (!round0 || f0) : (f0 != 0);
-    }
-    if (go) {
-        if (!DET) a.flag_cur[v] = 0;
-        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-        bool lower_changed = false;
-        BmVote st{cur, 0.0};
-        for (int64_t e = lo; e < hi; ++e) {
-            int32_t t = __ldg(&a.tgt[e]);
-            if (t == v) continue;
-            int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
-            st.acc(c, arc_weight<W>(a, e));
-        }
-        const int32_t cand = st.cand;
-        n_eval = 1;
-        n_arcs = (unsigned long long)(hi - lo);
-        if (DET) {
-            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
-            det_commit_output(a, v, cur, cand, T, lo, hi);
-        } else {
-            async_commit_output(a, v, cur, cand, lo, hi, n_delta);
-        }
-    }
-    warp_count(a.counters, n_eval, n_arcs, n_delta);
-}
-
-// High degree: one vote per chunk (each starts at (cur, 0)), reduce_votes
-// pair-max -- a total order, so the warp butterfly gives the same answer.
-template <class W, bool DET>
-__global__ void __launch_bounds__(kThreads) k_bm_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
-                                                    int round0) {
+__global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int round0) {
+    constexpr int S = WinS<W>::S;
+    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
+    __shared__ W s_w[kWinWarps][32][S + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
     if (wid >= count) return;
     const int32_t v = __ldg(&list[wid]);
     const uint8_t f0 = a.flag_cur[v];
@@ -370,17 +602,16 @@ __global__ void __launch_bounds__(kThreads) k_bm_hi(SweepArgs a, const int32_t *
     bool have = false;
     int32_t bc = 0;
     double bw = 0.0;
-    for (int p = lane; p < P; p += 32) {
-        int64_t s, e;
-        chunk_bounds(deg, P, p, s, e);
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
         BmVote st{cur, 0.0};
-        for (int64_t x = lo + s; x < lo + e; ++x) {
-            int32_t t = __ldg(&a.tgt[x]);
-            if (t == v) continue;
-            int32_t c = DET ? det_label(a, t, v, lower_changed) : async_label(a, t);
-            st.acc(c, arc_weight<W>(a, x));
-        }
-        if (!have || bm_better(st.w, st.cand, bw, bc)) { bc = st.cand; bw = st.w; have = true; }
+        window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
+                               [&](int64_t, bool valid, int32_t c, double w) {
+                                         if (valid) st.acc(c, w);
+                                     });
+        if (p < P && (!have || bm_better(st.w, st.cand, bw, bc))) { bc = st.cand; bw = st.w; have = true; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -452,47 +683,38 @@ __global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *
 }
 
 // ================================================================== round plumbing
-// Dirty bitmap -> next-round worklists, split by degree class; consumed
-// words are cleared so the same bitmap collects the following round.
-__global__ void __launch_bounds__(kThreads) k_compact(uint32_t *__restrict__ dirty, int64_t nwords,
-                                                      const uint8_t *__restrict__ cls, int32_t *__restrict__ wl_lo,
-                                                      int32_t *__restrict__ wl_hi,
-                                                      unsigned long long *__restrict__ counters) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t word = 0;
-    if (i < nwords) {
-        word = dirty[i];
-        if (word) dirty[i] = 0;
+// Next-round worklist = the entries of a degree-ordered bin whose dirty bit
+// is set (so re-evaluation warps stay degree-homogeneous and the longest
+// high-degree scans start first).  One atomic per block; order within a
+// block is kept.  The bitmap is cleared afterwards by a memset.
+__global__ void __launch_bounds__(kThreads) k_filter_dirty(const int32_t *__restrict__ bin, int64_t count,
+                                                           const uint32_t *__restrict__ dirty,
+                                                           int32_t *__restrict__ out,
+                                                           unsigned long long *__restrict__ cursor) {
+    __shared__ int s_warp[kThreads / 32];
+    __shared__ unsigned long long s_base;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t v = 0;
+    bool hit = false;
+    if (i < count) {
+        v = __ldg(&bin[i]);
+        hit = (__ldcg(&dirty[v >> 5]) >> (v & 31)) & 1u;
     }
-    int nlo = 0, nhi = 0;
-    for (uint32_t w = word; w; w &= w - 1) {
-        int32_t v = (int32_t)(i * 32 + (__ffs(w) - 1));
-        uint8_t c = cls[v];
-        nlo += c == CLS_LO;
-        nhi += c == CLS_HI;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s_warp[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int j = 0; j < kThreads / 32; ++j) {
+            int c = s_warp[j];
+            s_warp[j] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(cursor, (unsigned long long)tot) : 0ull;
     }
-    const int lane = threadIdx.x & 31;
-    int plo = nlo, phi = nhi;  // inclusive scans
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, plo, o);
-        int b = __shfl_up_sync(0xffffffffu, phi, o);
-        if (lane >= o) { plo += a; phi += b; }
-    }
-    unsigned long long blo = 0, bhi = 0;
-    int tlo = __shfl_sync(0xffffffffu, plo, 31), thi = __shfl_sync(0xffffffffu, phi, 31);
-    if (lane == 31) {
-        if (tlo) blo = atomicAdd(&counters[CNT_LO * CNT_STRIPES], (unsigned long long)tlo);
-        if (thi) bhi = atomicAdd(&counters[CNT_HI * CNT_STRIPES], (unsigned long long)thi);
-    }
-    blo = __shfl_sync(0xffffffffu, blo, 31) + (plo - nlo);
-    bhi = __shfl_sync(0xffffffffu, bhi, 31) + (phi - nhi);
-    for (uint32_t w = word; w; w &= w - 1) {
-        int32_t v = (int32_t)(i * 32 + (__ffs(w) - 1));
-        uint8_t c = cls[v];
-        if (c == CLS_LO) wl_lo[blo++] = v;
-        else if (c == CLS_HI) wl_hi[bhi++] = v;
-    }
+    __syncthreads();
+    if (hit) out[s_base + s_warp[w] + __popc(m & ((1u << lane) - 1))] = v;
 }
 
 // End of a deterministic sweep: fold L1 into L0, count ΔN, and set the
@@ -583,20 +805,29 @@ __global__ void k_sync_lab_new(const int32_t *lab_old, uint32_t *lab_new, int64_
 // ------------------------------------------------------------------ dispatch
 typedef void (*EvalKernel)(SweepArgs, const int32_t *, int64_t, int);
 
-struct KernelPair {
-    EvalKernel lo, hi;
+// lo: one lane per vertex, one sketch; mid: one lane per vertex, R_H chunks;
+// hi: one warp per vertex, lane = chunk (or thread-per-vertex for `exact`).
+struct KernelSet {
+    EvalKernel lo, mid, hi;
+    int lo_threads, hi_threads;
     bool hi_is_warp;
 };
 
 template <class W, bool DET>
-KernelPair pick_kernels(const slpa_config *cfg) {
-    if (cfg->variant == SLPA_VARIANT_EXACT) return {k_exact<W, DET>, k_exact<W, DET>, false};
-    if (cfg->variant == SLPA_VARIANT_BM) return {k_bm_lo<W, DET>, k_bm_hi<W, DET>, true};
-    if (cfg->sketch_slots == 8) return {k_mg_lo<W, 8, DET>, k_mg_hi<W, 8, DET>, true};
-    return {k_mg_lo<W, 0, DET>, k_mg_hi<W, 0, DET>, true};
+KernelSet pick_kernels(const slpa_config *cfg) {
+    if (cfg->variant == SLPA_VARIANT_EXACT)
+        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, kThreads, kThreads, false};
+    if (cfg->variant == SLPA_VARIANT_BM)
+        return {k_lane_win<W, BmLane<false>, DET>, k_lane_win<W, BmLane<true>, DET>, k_bm_hi_win<W, DET>, kWinThreads,
+                kWinThreads, true};
+    if (cfg->sketch_slots == 8)
+        return {k_lane_win<W, MgLane<8, false>, DET>, k_lane_win<W, MgLane<8, true>, DET>, k_mg_hi_win<W, 8, DET>,
+                kWinThreads, kWinThreads, true};
+    return {k_lane_win<W, MgLane<0, false>, DET>, k_lane_win<W, MgLane<0, true>, DET>, k_mg_hi_win<W, 0, DET>,
+            kWinThreads, kWinThreads, true};
 }
 
-KernelPair kernels_for(const slpa_ctx *ctx, const slpa_config *cfg, bool det) {
+KernelSet kernels_for(const slpa_ctx *ctx, const slpa_config *cfg, bool det) {
     if (ctx->g.w_f64) return det ? pick_kernels<double, true>(cfg) : pick_kernels<double, false>(cfg);
     return det ? pick_kernels<float, true>(cfg) : pick_kernels<float, false>(cfg);
 }
@@ -621,6 +852,8 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     a.parts = cfg->partial_groups;
     a.scan_double = cfg->scan_mode == SLPA_SCAN_DOUBLE;
     a.symmetric = g.symmetric;
+    a.thr = cfg->degree_threshold;
+    a.single = cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch;
     return a;
 }
 
@@ -660,25 +893,29 @@ void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn) {
     ctx->prof.arcs[cls] += (int64_t)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI] - a0);
 }
 
-void launch_lo(slpa_ctx *ctx, const KernelPair &kp, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
-               int cls) {
+void launch_lane(slpa_ctx *ctx, EvalKernel k, int threads, const SweepArgs &a, const int32_t *list, int64_t cnt,
+                 int round0, int cls) {
     if (cnt <= 0) return;
     timed_launch(ctx, cls, 1, [&] {
-        kp.lo<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+        k<<<grid_for(cnt, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
         CUDA_TRY(cudaGetLastError());
     });
 }
 
-void launch_hi(slpa_ctx *ctx, const KernelPair &kp, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
+void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
                int cls) {
     if (cnt <= 0) return;
     timed_launch(ctx, cls, 1, [&] {
-        if (kp.hi_is_warp)
-            kp.hi<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
-        else
-            kp.hi<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+        const int64_t items = ks.hi_is_warp ? cnt * 32 : cnt;
+        ks.hi<<<grid_for(items, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(a, list, cnt, round0);
         CUDA_TRY(cudaGetLastError());
     });
+}
+
+void launch_filter(cudaStream_t s, const int32_t *bin, int64_t count, const uint32_t *dirty, int32_t *out,
+                   unsigned long long *cursor) {
+    if (count <= 0) return;
+    k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor);
 }
 
 }  // namespace
@@ -689,42 +926,52 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     WorkBuffers &wb = ctx->wb;
     cudaStream_t s = ctx->stream;
     const int64_t n = g.n;
-    KernelPair kp = kernels_for(ctx, cfg, true);
-    SweepArgs a = make_args(ctx, cfg, pickless);
+    const KernelSet ks = kernels_for(ctx, cfg, true);
+    const SweepArgs a = make_args(ctx, cfg, pickless);
     CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(wb.flag_b.p, 0, (size_t)n, s));
     for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
     // round 0: every flagged vertex, straight from the degree bins
-    launch_lo(ctx, kp, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
-    launch_hi(ctx, kp, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+    launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+    launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
     int64_t rounds = 1;
     unsigned long long evals0 = 0, arcs0 = 0;
     bool first = true;
     const int64_t nwords = (n + 31) / 32;
+    unsigned long long *cur_lo = wb.counters.p + CNT_LO * CNT_STRIPES, *cur_mid = wb.counters.p + CNT_MID * CNT_STRIPES,
+                       *cur_hi = wb.counters.p + CNT_HI * CNT_STRIPES;
     for (;;) {
-        CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, 2 * CNT_STRIPES * sizeof(unsigned long long), s));
-        timed_launch(ctx, SLPA_PROF_COMPACT, 1, [&] {
-            k_compact<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, nwords, g.cls.p, wb.wl_lo.p,
-                                                                      wb.wl_hi.p, wb.counters.p);
+        CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
+        CUDA_TRY(cudaMemsetAsync(cur_mid, 0, sizeof(unsigned long long), s));
+        CUDA_TRY(cudaMemsetAsync(cur_hi, 0, sizeof(unsigned long long), s));
+        timed_launch(ctx, SLPA_PROF_COMPACT, (g.n_lo > 0) + (g.n_mid > 0) + (g.n_hi > 0), [&] {
+            launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_a.p, wb.wl_hi.p, cur_hi);
+            launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
+            launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_a.p, wb.wl_mid.p, cur_mid);
             CUDA_TRY(cudaGetLastError());
         });
+        CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (size_t)nwords * sizeof(uint32_t), s));
         read_counters(ctx);
         if (first) {
             evals0 = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
             arcs0 = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
             first = false;
         }
-        const int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nhi = (int64_t)ctx->h_sum[CNT_HI];
-        if (nlo == 0 && nhi == 0) break;
-        launch_hi(ctx, kp, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
-        launch_lo(ctx, kp, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
+        const int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
+                      nhi = (int64_t)ctx->h_sum[CNT_HI];
+        if (nlo == 0 && nmid == 0 && nhi == 0) break;
+        launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
+        launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
         ++rounds;
     }
     const unsigned long long evals = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
     const unsigned long long arcs = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
     // commit: L0 <- L1, delta, next-sweep flags
-    timed_launch(ctx, SLPA_PROF_COMMIT, (g.n_lo > 0) + (g.n_hi > 0), [&] {
+    timed_launch(ctx, SLPA_PROF_COMMIT, (g.n_lo > 0) + (g.n_mid > 0) + (g.n_hi > 0), [&] {
         if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
+        if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
         if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
         CUDA_TRY(cudaGetLastError());
     });
@@ -742,17 +989,20 @@ int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     DeviceGraph &g = ctx->g;
     WorkBuffers &wb = ctx->wb;
     cudaStream_t s = ctx->stream;
-    KernelPair kp = kernels_for(ctx, cfg, false);
-    SweepArgs a = make_args(ctx, cfg, pickless);
+    const KernelSet ks = kernels_for(ctx, cfg, false);
+    const SweepArgs a = make_args(ctx, cfg, pickless);
     CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
     for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
     // Higher-degree vertices first: they carry most arcs and the tail.
-    launch_hi(ctx, kp, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
-    launch_lo(ctx, kp, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
-    timed_launch(ctx, SLPA_PROF_OTHER, 1, [&] {
-        k_clear_isolated_flags<<<grid_for(g.n, kThreads), kThreads, 0, s>>>(wb.flag_a.p, g.cls.p, g.n);
-        CUDA_TRY(cudaGetLastError());
-    });
+    launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+    launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
+    launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    if (!ctx->part) {  // partitioned: remote entries hold outgoing marks, cleared after the exchange
+        timed_launch(ctx, SLPA_PROF_OTHER, 1, [&] {
+            k_clear_isolated_flags<<<grid_for(g.n, kThreads), kThreads, 0, s>>>(wb.flag_a.p, g.cls.p, g.n);
+            CUDA_TRY(cudaGetLastError());
+        });
+    }
     read_counters(ctx);
     const int64_t ev = (int64_t)(ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI]);
     const int64_t ar = (int64_t)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI]);

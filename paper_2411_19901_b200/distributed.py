@@ -1,0 +1,136 @@
+"""Multi-GPU label propagation: contiguous vertex ranges, one process (and
+one Engine) per GPU, label / mark exchange over torch.distributed (NCCL on
+GPUs; the exchange logic is backend-agnostic and is tested with gloo).
+
+Per sweep (the asynchronous model of the paper's multi-GPU extension,
+SURVEY §8(e)):
+
+1. every rank sweeps its own rows in place (libslpa_b200 ``slpa_part_sweep``)
+   reading its label replica -- remote labels are one exchange old;
+2. the owned label ranges are all-gathered into every replica;
+3. the flag arrays are max-reduced: a rank's remote entries carry the
+   "neighbour changed" marks of lpa.py:223 for vertices other ranks own;
+   ``slpa_part_end_exchange`` then clears the remote entries;
+4. delta (changed vertices) is summed; the convergence test is lpa.py:299.
+
+The collectives operate on zero-copy torch views of the library's device
+buffers (``Engine.part_buffers``); torch is the plumbing, the sweep is the
+library's CUDA code.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def partition_ranges(n: int, world: int, degrees=None):
+    """Contiguous [begin, end) vertex ranges.  Balanced by arc count when
+    per-vertex degrees are given, else by vertex count."""
+    if world <= 0:
+        raise ValueError("world must be positive")
+    if degrees is None:
+        step = -(-n // world)
+        return [(min(n, r * step), min(n, (r + 1) * step)) for r in range(world)]
+    cum = np.concatenate([[0], np.cumsum(np.asarray(degrees, dtype=np.int64))])
+    total = int(cum[-1])
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")))
+    cuts.append(n)
+    cuts = np.maximum.accumulate(np.clip(cuts, 0, n))
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+class Exchange:
+    """Label all-gather + flag max-reduction over torch.distributed."""
+
+    def __init__(self, ranges, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.ranges = ranges
+        self.world = len(ranges)
+        self.rank = dist.get_rank(group)
+        self.maxlen = max(max(e - b for b, e in ranges), 1)
+        self._send = None
+        self._recv = None
+
+    def labels(self, lab):
+        import torch
+        if self._send is None or self._send.device != lab.device:
+            self._send = torch.zeros(self.maxlen, dtype=lab.dtype, device=lab.device)
+            self._recv = [torch.zeros(self.maxlen, dtype=lab.dtype, device=lab.device) for _ in range(self.world)]
+        b, e = self.ranges[self.rank]
+        self._send[: e - b].copy_(lab[b:e])
+        self.dist.all_gather(self._recv, self._send, group=self.group)
+        for r, (rb, re) in enumerate(self.ranges):
+            if r != self.rank and re > rb:
+                lab[rb:re].copy_(self._recv[r][: re - rb])
+
+    def flags(self, fl):
+        self.dist.all_reduce(fl, op=self.dist.ReduceOp.MAX, group=self.group)
+
+    def sum(self, x: int, device) -> int:
+        import torch
+        t = torch.tensor([int(x)], dtype=torch.int64, device=device)
+        self.dist.all_reduce(t, group=self.group)
+        return int(t.item())
+
+    def sum_f64(self, x: float, device) -> float:
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+
+@dataclass
+class PartitionedResult:
+    iterations: int
+    delta_history: list = field(default_factory=list)
+    converged: bool = False
+
+
+def _sync(t):
+    if getattr(t, "is_cuda", False):
+        import torch
+        torch.cuda.current_stream(t.device).synchronize()
+
+
+def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) -> PartitionedResult:
+    """lpa_run (lpa.py:262-308) over the ranks of `group`; `engine` holds this
+    rank's rows (Engine.part_gen_rmat / part_upload).  cfg.worker_count must
+    be > 0 (the asynchronous sweep)."""
+    cfg.validate()
+    ex = Exchange(ranges, group)
+    n = engine.n
+    engine.part_begin(cfg)
+    lab, fl = engine.part_buffers()
+    history = []
+    converged = False
+    for it in range(cfg.max_iterations):
+        pickless = (it % cfg.pickless_gap) == 0
+        local = engine.part_sweep(cfg, pickless)  # returns after its stream drained
+        ex.labels(lab)
+        ex.flags(fl)
+        _sync(lab)  # collectives on torch's stream finish before the library touches the buffers
+        engine.part_end_exchange()
+        delta = ex.sum(local, lab.device)
+        history.append(delta)
+        if iteration_hook is not None:
+            iteration_hook(it, pickless, lab)
+        if not pickless and (delta / n if n else 0.0) < cfg.tolerance:
+            converged = True
+            break
+    return PartitionedResult(len(history), history, converged)
+
+
+def modularity_partitioned(engine, ranges, group=None) -> float:
+    """metrics.py:63-74 over a partition: rank-local tallies, incident
+    all-reduced, internal weight summed."""
+    ex = Exchange(ranges, group)
+    internal, incident, _sizes = engine.part_tally()
+    ex.dist.all_reduce(incident, group=group)
+    total_internal = ex.sum_f64(internal, incident.device)
+    return engine.part_modularity(total_internal)

@@ -252,10 +252,89 @@ class Engine:
             sizes, internal, incident = sizes[: self.n], internal[: self.n], incident[: self.n]
         return (None if q is None else q.value), nc.value, sizes, internal, incident
 
+    # ------------------------------------------------------------------ partition (multi-GPU)
+    def part_gen_rmat(self, scale, v_begin, v_end, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, permute=True,
+                      perm_key=7):
+        """This rank's rows [v_begin, v_end) of the RMAT graph gen_rmat builds."""
+        ta, tab, tabc = rmat_thresholds(a, b, c)
+        rc = self.lib.slpa_part_gen_rmat(self.ctx, int(scale), int(edge_factor) << int(scale), ta, tab, tabc,
+                                         int(seed), 1 if permute else 0, int(perm_key), int(v_begin), int(v_end))
+        check(self.lib, self.ctx, rc)
+        return self._part_refresh()
+
+    def part_upload(self, n, v_begin, v_end, row_offsets, targets, weights):
+        """Rows [v_begin, v_end): row_offsets int64[v_end-v_begin+1] (from 0),
+        targets int32 (global ids), weights float32|float64."""
+        ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        tg = np.ascontiguousarray(targets, dtype=np.int32)
+        w = np.ascontiguousarray(weights)
+        if w.dtype not in (np.float32, np.float64):
+            w = w.astype(np.float64)
+        rc = self.lib.slpa_part_upload(self.ctx, int(n), int(v_begin), int(v_end), ro.ctypes.data, tg.ctypes.data,
+                                       w.ctypes.data, 1 if w.dtype == np.float64 else 0)
+        check(self.lib, self.ctx, rc)
+        return self._part_refresh()
+
+    def _part_refresh(self):
+        n, m, vb, ve = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib, self.ctx, self.lib.slpa_part_info(self.ctx, ctypes.byref(n), ctypes.byref(m),
+                                                          ctypes.byref(vb), ctypes.byref(ve)))
+        self.n, self.m, self.v_begin, self.v_end = n.value, m.value, vb.value, ve.value
+        return self
+
+    def part_begin(self, cfg):
+        c = config_struct(cfg)
+        check(self.lib, self.ctx, self.lib.slpa_part_begin(self.ctx, ctypes.byref(c)))
+
+    def part_sweep(self, cfg, pickless) -> int:
+        c = config_struct(cfg)
+        ch = ctypes.c_int64(0)
+        check(self.lib, self.ctx, self.lib.slpa_part_sweep(self.ctx, ctypes.byref(c), 1 if pickless else 0,
+                                                           ctypes.byref(ch)))
+        return int(ch.value)
+
+    def part_end_exchange(self):
+        check(self.lib, self.ctx, self.lib.slpa_part_end_exchange(self.ctx))
+
+    def part_buffers(self):
+        """(labels, flags) as zero-copy torch CUDA tensors over the context's
+        label replica (int32[n]) and flag array (uint8[n])."""
+        lp, fp = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        check(self.lib, self.ctx, self.lib.slpa_part_buffers(self.ctx, ctypes.byref(lp), ctypes.byref(fp)))
+        return (device_tensor(lp.value, self.n, "<i4", self.device), device_tensor(fp.value, self.n, "|u1", self.device))
+
+    def part_tally(self):
+        """(internal weight of owned rows, incident float64[n] tensor, sizes int64[n] tensor)."""
+        iw = ctypes.c_double(0.0)
+        ip, sp = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        check(self.lib, self.ctx, self.lib.slpa_part_tally(self.ctx, ctypes.byref(iw), ctypes.byref(ip),
+                                                           ctypes.byref(sp)))
+        return (iw.value, device_tensor(ip.value, self.n, "<f8", self.device),
+                device_tensor(sp.value, self.n, "<i8", self.device))
+
+    def part_modularity(self, internal_total) -> float:
+        q = ctypes.c_double(0.0)
+        rc = self.lib.slpa_part_modularity(self.ctx, float(internal_total), ctypes.byref(q))
+        check(self.lib, self.ctx, rc)
+        return q.value
+
     def stream(self) -> int:
         s = ctypes.c_uint64(0)
         check(self.lib, self.ctx, self.lib.slpa_stream(self.ctx, ctypes.byref(s)))
         return s.value
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of device memory owned by the library."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_tensor(ptr, n, typestr, device):
+    import torch
+    return torch.as_tensor(_CudaArray(ptr, n, typestr), device=f"cuda:{device}")
 
 
 def rmat_thresholds(a, b, c):

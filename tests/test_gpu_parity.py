@@ -257,7 +257,12 @@ def test_async_quality_within_tolerance(slpa, eng, oracle, kind):
     q_ref = oracle.modularity(g, ref.labels)
     res = slpa.lpa_run(g, slpa.LpaConfig(worker_count=1), engine=eng)
     q = slpa.modularity(g, res.labels, engine=eng)
-    assert abs(q - q_ref) <= 0.01 + 0.02 * (kind == "grid"), (q, q_ref)
+    if kind == "grid":
+        # permuted grids are schedule-sensitive (Jacobi 0.8205
+        # vs sequential 0.7697); async must not be worse than 1% absolute.
+        assert q >= q_ref - 0.01, (q, q_ref)
+    else:
+        assert abs(q - q_ref) <= 0.01, (q, q_ref)
     assert res.iterations <= 20
     assert res.labels.min() >= 0 and res.labels.max() < g.num_vertices
 
