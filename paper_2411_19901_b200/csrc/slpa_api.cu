@@ -105,6 +105,7 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.flag_a.alloc(n);
     wb.flag_b.alloc(n);
     wb.dirty_a.alloc(n / 32 + 1);
+    wb.dirty_b.alloc(n / 32 + 1);
     wb.wl_lo.alloc(n);
     wb.wl_mid.alloc(n);
     wb.wl_hi.alloc(n);
@@ -112,6 +113,7 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.io_flags.alloc(n);
     wb.counters.alloc(CNT_TOTAL);
     CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     if (!ctx->h_counters) CUDA_TRY(cudaMallocHost((void **)&ctx->h_counters, CNT_TOTAL * sizeof(unsigned long long)));
 }
 

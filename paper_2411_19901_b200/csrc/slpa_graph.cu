@@ -90,6 +90,29 @@ __global__ void k_fill_reverse(const int64_t *off, const int32_t *tgt, int64_t n
         }
 }
 
+// ------------------------------------------------------------------ integer precondition
+// Every weight an integer >= 1 and every weighted degree < 2^31: then all
+// sketch / vote values are integers < 2^31 and uint32 arithmetic reproduces
+// the reference's binary64 arithmetic exactly.
+template <class W>
+__global__ void k_int_check(const int64_t *off, const W *w, int64_t n, unsigned *bad) {
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+        double sum = 0.0;
+        bool ok = true;
+        for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+            const double x = (double)w[e];
+            ok &= (x >= 1.0) && (x == floor(x)) && (x < 2147483648.0);
+            sum += x;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        ok = __all_sync(0xffffffffu, ok) && sum < 2147483648.0;
+        if (!ok && lane == 0) atomicOr(bad, 1u);
+    }
+}
+
 // ------------------------------------------------------------------ order
 __global__ void k_order_scatter(const int64_t *order, int64_t n, int32_t *ids, int32_t *pos, unsigned *seen,
                                 unsigned *err) {
@@ -387,6 +410,23 @@ void slpa_graph_validate(slpa_ctx *ctx, const Csr &c, int w_f64) {
     if (e & 16) throw SlpaError{SLPA_EINVAL, "arc weights must be positive"};
 }
 
+void slpa_check_int_weights(slpa_ctx *ctx) {
+    DeviceGraph &g = ctx->g;
+    cudaStream_t s = ctx->stream;
+    g.int_weights = 1;
+    if (g.n == 0 || g.m == 0) return;
+    DevBuf<unsigned> bad;
+    bad.alloc(1);
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0, sizeof(unsigned), s));
+    if (g.w_f64)
+        k_int_check<double><<<grid_warps(g.n), kT, 0, s>>>(g.off(), (const double *)g.w(), g.n, bad.p);
+    else
+        k_int_check<float><<<grid_warps(g.n), kT, 0, s>>>(g.off(), (const float *)g.w(), g.n, bad.p);
+    CUDA_TRY(cudaGetLastError());
+    g.int_weights = read_flag(ctx, bad.p) == 0;
+    bad.release();
+}
+
 // Symmetry check + reverse CSR of the active numbering; resets the bins.
 void slpa_graph_finalize(slpa_ctx *ctx) {
     DeviceGraph &g = ctx->g;
@@ -397,6 +437,7 @@ void slpa_graph_finalize(slpa_ctx *ctx) {
     g.roff.release();
     g.rsrc.release();
     g.symmetric = 1;
+    slpa_check_int_weights(ctx);
     if (g.n == 0 || g.m == 0) return;
     DevBuf<unsigned long long> acc;
     acc.alloc(4);

@@ -82,6 +82,7 @@ struct SweepArgs {
     int32_t symmetric;
     int32_t thr;                      // degree_threshold (chunked evaluation at deg >= thr)
     int32_t single;                   // shared_sketch: one sketch over any degree
+    int32_t dbg;                      // timing experiments only (SLPA_DEBUG_SKIP); 0 in production
 };
 
 enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_N = 8 };
@@ -103,6 +104,7 @@ struct DeviceGraph {
     int32_t w_f64 = 0;
     int32_t symmetric = 1;
     int32_t has_order = 0;
+    int32_t int_weights = 0;  // exactness precondition for integer sketch values
     Csr base;              // original ids (as uploaded / generated)
     Csr perm;              // visiting-order positions (has_order only)
     DevBuf<int32_t> ids;   // position -> id (has_order)

@@ -15,6 +15,7 @@
 #include "slpa_internal.cuh"
 
 void slpa_graph_validate(slpa_ctx *ctx, const Csr &c, int w_f64);
+void slpa_check_int_weights(slpa_ctx *ctx);
 void slpa_part_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
                              uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t r0,
                              int64_t r1);
@@ -57,6 +58,7 @@ void mark_partitioned(slpa_ctx *ctx, int64_t vb, int64_t ve) {
     g.roff.release();
     g.rsrc.release();
     g.symmetric = 1;  // only the asynchronous sweep runs partitioned
+    slpa_check_int_weights(ctx);
     g.bin_thr = -1;
     g.bin_single = -1;
     g.bin_lo_sorted = -1;

@@ -1,7 +1,15 @@
 // slpa_sketch.cuh -- register-resident weighted Misra-Gries sketch and weighted
-// Boyer-Moore vote, with exactly the reference's slot rules and binary64
-// arithmetic (sketch.py:17-181), plus the warp-cooperative slot-parallel
-// merge used by the high-degree path.
+// Boyer-Moore vote, with exactly the reference's slot rules (sketch.py:17-181),
+// plus the warp-cooperative slot-parallel merge of the high-degree path.
+//
+// Value type V:
+//   double   -- the reference's binary64 arithmetic, any positive weights;
+//   uint32_t -- used only when every weight is an integer and every weighted
+//               degree is < 2^31 (checked on the device at upload).  Then every
+//               sketch / vote value is an integer in [0, weighted degree], so
+//               binary64 add / subtract / compare are exact and the integer
+//               sketch is bit-identical -- with a shorter
+//               dependency chain and half the value registers.
 #pragma once
 #include "slpa_internal.cuh"
 
@@ -10,78 +18,83 @@ struct KArr {
     static constexpr int v = K > 0 ? K : SLPA_KDYN;
 };
 
+template <class V>
+__device__ __forceinline__ V clamp_sub(V v, V w) {  // max(v - w, 0) as sketch.py:73
+    if constexpr (sizeof(V) == 4) return v > w ? v - w : (V)0;
+    else {
+        V t = v - w;
+        return t > (V)0 ? t : (V)0;
+    }
+}
+
 // MgSketch (sketch.py:17-137).  K > 0: compile-time slots (registers);
 // K == 0: runtime k <= SLPA_KDYN (local memory).
-template <int K>
+template <int K, class V = double>
 struct MgSketchDev {
     int32_t key[KArr<K>::v];
-    double val[KArr<K>::v];
+    V val[KArr<K>::v];
 
     __device__ __forceinline__ void reset(int k) {  // MgSketch.__init__ sketch.py:34-39
         if constexpr (K > 0) {
 #pragma unroll
-            for (int i = 0; i < K; ++i) { key[i] = 0; val[i] = 0.0; }
+            for (int i = 0; i < K; ++i) { key[i] = 0; val[i] = (V)0; }
         } else {
-            for (int i = 0; i < k; ++i) { key[i] = 0; val[i] = 0.0; }
+            for (int i = 0; i < k; ++i) { key[i] = 0; val[i] = (V)0; }
         }
     }
 
     // accumulate (sketch.py:47-74): first slot whose key equals c (stale keys
-    // included) gains w; else the first slot with value 0.0 takes (c, w); else
+    // included) gains w; else the first slot with value 0 takes (c, w); else
     // every slot loses w, clamped at 0.
-    __device__ __forceinline__ void acc(int32_t c, double w, int k) {
+    __device__ __forceinline__ void acc(int32_t c, V w, int k) {
         if constexpr (K > 0) {
-            int hit = -1, fr = -1;
+            unsigned mm = 0, fm = 0;
 #pragma unroll
-            for (int i = K - 1; i >= 0; --i) {
-                if (key[i] == c) hit = i;
-                if (val[i] == 0.0) fr = i;
+            for (int i = 0; i < K; ++i) {
+                mm |= (unsigned)(key[i] == c) << i;
+                fm |= (unsigned)(val[i] == (V)0) << i;
             }
-            if (hit >= 0) {
+            if (mm) {
+                const unsigned sel = mm & (0u - mm);
 #pragma unroll
                 for (int i = 0; i < K; ++i)
-                    if (i == hit) val[i] += w;
-            } else if (fr >= 0) {
+                    if (sel & (1u << i)) val[i] += w;
+            } else if (fm) {
+                const unsigned sel = fm & (0u - fm);
 #pragma unroll
                 for (int i = 0; i < K; ++i)
-                    if (i == fr) { key[i] = c; val[i] = w; }
+                    if (sel & (1u << i)) { key[i] = c; val[i] = w; }
             } else {
 #pragma unroll
-                for (int i = 0; i < K; ++i) {
-                    double t = val[i] - w;
-                    val[i] = t > 0.0 ? t : 0.0;
-                }
+                for (int i = 0; i < K; ++i) val[i] = clamp_sub(val[i], w);
             }
         } else {
             for (int i = 0; i < k; ++i)
                 if (key[i] == c) { val[i] += w; return; }
             for (int i = 0; i < k; ++i)
-                if (val[i] == 0.0) { key[i] = c; val[i] = w; return; }
-            for (int i = 0; i < k; ++i) {
-                double t = val[i] - w;
-                val[i] = t > 0.0 ? t : 0.0;
-            }
+                if (val[i] == (V)0) { key[i] = c; val[i] = w; return; }
+            for (int i = 0; i < k; ++i) val[i] = clamp_sub(val[i], w);
         }
     }
 
     __device__ __forceinline__ void clear_values(int k) {  // sketch.py:107-111
         if constexpr (K > 0) {
 #pragma unroll
-            for (int i = 0; i < K; ++i) val[i] = 0.0;
+            for (int i = 0; i < K; ++i) val[i] = (V)0;
         } else {
-            for (int i = 0; i < k; ++i) val[i] = 0.0;
+            for (int i = 0; i < k; ++i) val[i] = (V)0;
         }
     }
 
-    __device__ __forceinline__ void rescan_add(int32_t c, double w, int k) {  // sketch.py:113-126
+    __device__ __forceinline__ void rescan_add(int32_t c, V w, int k) {  // sketch.py:113-126
         if constexpr (K > 0) {
-            int hit = -1;
+            unsigned mm = 0;
 #pragma unroll
-            for (int i = K - 1; i >= 0; --i)
-                if (key[i] == c) hit = i;
+            for (int i = 0; i < K; ++i) mm |= (unsigned)(key[i] == c) << i;
+            const unsigned sel = mm & (0u - mm);
 #pragma unroll
             for (int i = 0; i < K; ++i)
-                if (i == hit) val[i] += w;
+                if (sel & (1u << i)) val[i] += w;
         } else {
             for (int i = 0; i < k; ++i)
                 if (key[i] == c) { val[i] += w; return; }
@@ -92,13 +105,13 @@ struct MgSketchDev {
     __device__ __forceinline__ bool max_key(int k, int32_t &out) const {
         bool found = false;
         int32_t best = 0;
-        double bw = 0.0;
+        V bw = (V)0;
         const int kk = K > 0 ? K : k;
 #pragma unroll
         for (int i = 0; i < KArr<K>::v; ++i) {
             if (K == 0 && i >= kk) break;
-            double v = val[i];
-            if (v > 0.0) {
+            V v = val[i];
+            if (v > (V)0) {
                 int32_t c = key[i];
                 if (!found || v > bw || (v == bw && c < best)) { best = c; bw = v; found = true; }
             }
@@ -109,10 +122,11 @@ struct MgSketchDev {
 };
 
 // BmState (sketch.py:140-162)
+template <class V = double>
 struct BmVote {
     int32_t cand;
-    double w;
-    __device__ __forceinline__ void acc(int32_t c, double x) {
+    V w;
+    __device__ __forceinline__ void acc(int32_t c, V x) {
         if (c == cand) w += x;
         else if (w > x) w -= x;
         else { cand = c; w = x; }
@@ -120,7 +134,8 @@ struct BmVote {
 };
 
 // reduce_votes order (sketch.py:165-181): max weight, ties to smaller candidate.
-__device__ __forceinline__ bool bm_better(double w1, int32_t c1, double w0, int32_t c0) {
+template <class V>
+__device__ __forceinline__ bool bm_better(V w1, int32_t c1, V w0, int32_t c0) {
     return w1 > w0 || (w1 == w0 && c1 < c0);
 }
 
@@ -136,41 +151,40 @@ __device__ __forceinline__ void chunk_bounds(int64_t count, int64_t parts, int64
 // (lane l < k holds slot l).  `acc` replays MgSketch.accumulate with the
 // physical slot rules: first matching lane (ballot + ffs), else first empty
 // lane, else every lane decrements.  (c, w) must be warp-uniform.
+template <class V = double>
 struct WarpSketch {
     int32_t key;
-    double val;
-    __device__ __forceinline__ void acc(int lane, int k, int32_t c, double w) {
+    V val;
+    __device__ __forceinline__ void acc(int lane, int k, int32_t c, V w) {
         const bool live = lane < k;
-        unsigned mm = __ballot_sync(0xffffffffu, live && key == c);
+        const unsigned mm = __ballot_sync(0xffffffffu, live && key == c);
+        const unsigned fm = __ballot_sync(0xffffffffu, live && val == (V)0);
         if (mm) {
             if (lane == __ffs(mm) - 1) val += w;
-            return;
-        }
-        unsigned fm = __ballot_sync(0xffffffffu, live && val == 0.0);
-        if (fm) {
+        } else if (fm) {
             if (lane == __ffs(fm) - 1) { key = c; val = w; }
-            return;
-        }
-        if (live) {
-            double t = val - w;
-            val = t > 0.0 ? t : 0.0;
+        } else if (live) {
+            val = clamp_sub(val, w);
         }
     }
-    __device__ __forceinline__ void rescan_add(int lane, int k, int32_t c, double w) {
+    __device__ __forceinline__ void rescan_add(int lane, int k, int32_t c, V w) {
         unsigned mm = __ballot_sync(0xffffffffu, lane < k && key == c);
         if (mm && lane == __ffs(mm) - 1) val += w;
     }
     // max_key over the lanes; result valid on every lane.
     __device__ __forceinline__ bool max_key(int lane, int k, int32_t &out) const {
-        double bw = (lane < k && val > 0.0) ? val : -1.0;
+        const bool have = lane < k && val > (V)0;
+        V bw = have ? val : (V)0;
         int32_t bk = key;
+        int hv = have;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            double ow = __shfl_xor_sync(0xffffffffu, bw, o);
+            V ow = __shfl_xor_sync(0xffffffffu, bw, o);
             int32_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            if (ow > bw || (ow == bw && ok < bk)) { bw = ow; bk = ok; }
+            int oh = __shfl_xor_sync(0xffffffffu, hv, o);
+            if (oh && (!hv || ow > bw || (ow == bw && ok < bk))) { bw = ow; bk = ok; hv = 1; }
         }
         out = bk;
-        return bw > 0.0;
+        return hv != 0;
     }
 };

@@ -19,6 +19,7 @@
 //   * L1 and the changed bit share one 32-bit word (bit 31), so a single
 //     gather of a lower neighbour gives its label and whether it changed.
 // Async mode (worker_count > 0) is the paper's in-place parallel sweep.
+#include <cstdlib>
 #include "slpa_sketch.cuh"
 #include "slpa_internal.cuh"
 
@@ -294,7 +295,7 @@ __device__ __forceinline__ void window_streams(const SweepArgs &a, uint32_t (*s_
             const uint32_t L = s_lab[lane][x];
             const bool valid = w != (W)0;
             lower_changed |= valid && (L >> 31) != 0;
-            consume(s0 + x, valid, (int32_t)(L & SLPA_LMASK), (double)w);
+            consume(s0 + x, valid, (int32_t)(L & SLPA_LMASK), w);
         }
         __syncwarp();
     }
@@ -341,10 +342,10 @@ __device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t
 // are cut by arc position while the row streams; each finished chunk is
 // folded into parts[0] right away -- the same replay sequence as
 // sk = parts[0]; sk.merge(parts[1]); ... (lpa.py:179-186, sketch.py:76-91).
-template <int K, bool CHUNKED>
+template <int K, bool CHUNKED, class V>
 struct MgLane {
     static constexpr bool kHasRescan = true;
-    MgSketchDev<K> S, part;
+    MgSketchDev<K, V> S, part;
     int k, p;
     int64_t base, rem, next;
     __device__ __forceinline__ void init(int k_, int32_t, int64_t deg, int P) {
@@ -365,26 +366,28 @@ struct MgLane {
 #pragma unroll
             for (int i = 0; i < KArr<K>::v; ++i) {
                 if (K == 0 && i >= k) break;
-                if (part.val[i] > 0.0) S.acc(part.key[i], part.val[i], k);
+                if (part.val[i] > (V)0) S.acc(part.key[i], part.val[i], k);
             }
         }
         part.reset(k);
         ++p;
         next += base + (p < rem ? 1 : 0);
     }
-    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, double w) {
+    template <class W>
+    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, W w) {
         if (CHUNKED) {
             if (pos == next) end_chunk();
-            if (valid) part.acc(c, w, k);
+            if (valid) part.acc(c, (V)w, k);
         } else if (valid) {
-            S.acc(c, w, k);
+            S.acc(c, (V)w, k);
         }
     }
     __device__ __forceinline__ void finish() {
         if (CHUNKED) end_chunk();
     }
     __device__ __forceinline__ void rescan_begin() { S.clear_values(k); }
-    __device__ __forceinline__ void rescan(int32_t c, double w) { S.rescan_add(c, w, k); }
+    template <class W>
+    __device__ __forceinline__ void rescan(int32_t c, W w) { S.rescan_add(c, (V)w, k); }
     __device__ __forceinline__ int32_t result(int32_t cur) const {
         int32_t b;
         return S.max_key(k, b) ? b : cur;  // lpa.py:192-193
@@ -393,16 +396,16 @@ struct MgLane {
 
 // BM over one row: one BmState(cur, 0) per chunk, reduce_votes pair-max
 // (lpa.py:137-150); unchunked rows are a single vote.
-template <bool CHUNKED>
+template <bool CHUNKED, class V>
 struct BmLane {
     static constexpr bool kHasRescan = false;
-    BmVote st, best;
+    BmVote<V> st, best;
     int32_t cur0;
     int p;
     int64_t base, rem, next;
     __device__ __forceinline__ void init(int, int32_t cur, int64_t deg, int P) {
         cur0 = cur;
-        st = BmVote{cur, 0.0};
+        st = BmVote<V>{cur, (V)0};
         if (CHUNKED) {
             p = 0;
             base = deg / P;
@@ -412,20 +415,22 @@ struct BmLane {
     }
     __device__ __forceinline__ void end_chunk() {
         if (p == 0 || bm_better(st.w, st.cand, best.w, best.cand)) best = st;
-        st = BmVote{cur0, 0.0};
+        st = BmVote<V>{cur0, (V)0};
         ++p;
         next += base + (p < rem ? 1 : 0);
     }
-    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, double w) {
+    template <class W>
+    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, W w) {
         if (CHUNKED && pos == next) end_chunk();
-        if (valid) st.acc(c, w);
+        if (valid) st.acc(c, (V)w);
     }
     __device__ __forceinline__ void finish() {
         if (CHUNKED) end_chunk();
         else best = st;
     }
     __device__ __forceinline__ void rescan_begin() {}
-    __device__ __forceinline__ void rescan(int32_t, double) {}
+    template <class W>
+    __device__ __forceinline__ void rescan(int32_t, W) {}
     __device__ __forceinline__ int32_t result(int32_t) const { return best.cand; }
 };
 
@@ -457,13 +462,13 @@ __global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int
     pol.init(a.k, cur, deg, a.parts);
     bool lower_changed = false;
     window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, lower_changed,
-                                  [&](int64_t pos, bool valid, int32_t c, double w) { pol.on(pos, valid, c, w); });
+                                  [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
     if (go && deg) pol.finish();
     if (Pol::kHasRescan && a.scan_double) {
         pol.rescan_begin();
         bool dummy = false;
         window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, dummy,
-                                      [&](int64_t, bool valid, int32_t c, double w) {
+                                      [&](int64_t, bool valid, int32_t c, W w) {
                                           if (valid) pol.rescan(c, w);
                                       });
     }
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int
 // R_H) (lpa.py:178-183) with a register sketch, streamed through the window
 // tile; then parts[1..] are replayed into parts[0] in order (sketch.py:
 // 76-91) on a slot-parallel warp sketch (lane l = slot l).
-template <class W, int K, bool DET>
+template <class W, int K, bool DET, class V>
 __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const int32_t *__restrict__ list,
                                                            int64_t count, int round0) {
     constexpr int S = WinS<W>::S;
@@ -502,16 +507,16 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
     const int k = K > 0 ? K : a.k;
     const int P = a.parts;
     bool lower_changed = false;
-    WarpSketch S_{0, 0.0};
+    WarpSketch<V> S_{0, (V)0};
     for (int b0 = 0; b0 < P; b0 += 32) {
         const int p = b0 + lane;
-        MgSketchDev<K> part;
+        MgSketchDev<K, V> part;
         part.reset(k);
         int64_t cs = 0, ce = 0;
         if (p < P) chunk_bounds(deg, P, p, cs, ce);
         window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
                                [&](int64_t, bool valid, int32_t c, double w) {
-                                         if (valid) part.acc(c, w, k);
+                                         if (valid && !(a.dbg & 2)) part.acc(c, w, k);
                                      });
         int first = 0;
         if (b0 == 0) {  // sk = parts[0]
@@ -519,7 +524,7 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
             for (int i = 0; i < KArr<K>::v; ++i) {
                 if (K == 0 && i >= k) break;
                 int32_t kk = __shfl_sync(0xffffffffu, part.key[i], 0);
-                double vv = __shfl_sync(0xffffffffu, part.val[i], 0);
+                V vv = __shfl_sync(0xffffffffu, part.val[i], 0);
                 if (lane == i) { S_.key = kk; S_.val = vv; }
             }
             first = 1;
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
 #pragma unroll
         for (int i = 0; i < KArr<K>::v; ++i) {
             if (K == 0 && i >= k) break;
-            if (part.val[i] > 0.0) nz |= 1u << (i & 31);
+            if (part.val[i] > (V)0) nz |= 1u << (i & 31);
         }
         for (int q = first; q < nb; ++q) {
             const unsigned mq = __shfl_sync(0xffffffffu, nz, q);
@@ -539,25 +544,25 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
                 if (K == 0 && i >= k) break;
                 if (!(mq & (1u << (i & 31)))) continue;
                 int32_t c = __shfl_sync(0xffffffffu, part.key[i], q);
-                double w = __shfl_sync(0xffffffffu, part.val[i], q);
-                S_.acc(lane, k, c, w);
+                V w = __shfl_sync(0xffffffffu, part.val[i], q);
+                if (!(a.dbg & 1)) S_.acc(lane, k, c, w);
             }
         }
     }
     if (a.scan_double) {  // exact per-key re-count in adjacency order
-        S_.val = 0.0;
+        S_.val = (V)0;
         bool dummy = false;
         for (int64_t base = lo; base < hi; base += 32) {
             int64_t x = base + lane;
             int32_t c = 0;
-            double w = 0.0;
+            V w = (V)0;
             bool ok = false;
             if (x < hi) {
                 int32_t t = __ldg(&a.tgt[x]);
                 if (t != v) {
                     ok = true;
                     c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
-                    w = arc_weight<W>(a, x);
+                    w = (V)arc_weight<W>(a, x);
                 }
             }
             unsigned okm = __ballot_sync(0xffffffffu, ok);
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
                 int j = __ffs(okm) - 1;
                 okm &= okm - 1;
                 int32_t cj = __shfl_sync(0xffffffffu, c, j);
-                double wj = __shfl_sync(0xffffffffu, w, j);
+                V wj = __shfl_sync(0xffffffffu, w, j);
                 S_.rescan_add(lane, k, cj, wj);
             }
         }
@@ -576,7 +581,7 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
 }
 
 // High degree, BM: one vote per chunk, pair-max reduce (lpa.py:143-150).
-template <class W, bool DET>
+template <class W, bool DET, class V>
 __global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const int32_t *__restrict__ list,
                                                            int64_t count, int round0) {
     constexpr int S = WinS<W>::S;
@@ -601,12 +606,12 @@ __global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const in
     bool lower_changed = false;
     bool have = false;
     int32_t bc = 0;
-    double bw = 0.0;
+    V bw = (V)0;
     for (int b0 = 0; b0 < P; b0 += 32) {
         const int p = b0 + lane;
         int64_t cs = 0, ce = 0;
         if (p < P) chunk_bounds(deg, P, p, cs, ce);
-        BmVote st{cur, 0.0};
+        BmVote<V> st{cur, (V)0};
         window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
                                [&](int64_t, bool valid, int32_t c, double w) {
                                          if (valid) st.acc(c, w);
@@ -617,7 +622,7 @@ __global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const in
     for (int o = 16; o > 0; o >>= 1) {
         int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
         int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        double ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        V ow = __shfl_xor_sync(0xffffffffu, bw, o);
         if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
     }
     warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
@@ -683,6 +688,17 @@ __global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *
 }
 
 // ================================================================== round plumbing
+// Deferred heavy (mid / hi) vertices: their dirty bits move to a persistent
+// pending bitmap and are only re-evaluated once the light vertices are quiet.
+__global__ void __launch_bounds__(kThreads) k_defer_dirty(const int32_t *__restrict__ bin, int64_t count,
+                                                          const uint32_t *__restrict__ dirty,
+                                                          uint32_t *__restrict__ pend) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int32_t v = __ldg(&bin[i]);
+    if ((__ldcg(&dirty[v >> 5]) >> (v & 31)) & 1u) atomicOr(&pend[v >> 5], 1u << (v & 31));
+}
+
 // Next-round worklist = the entries of a degree-ordered bin whose dirty bit
 // is set (so re-evaluation warps stay degree-homogeneous and the longest
 // high-degree scans start first).  One atomic per block; order within a
@@ -813,23 +829,33 @@ struct KernelSet {
     bool hi_is_warp;
 };
 
-template <class W, bool DET>
+template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
     if (cfg->variant == SLPA_VARIANT_EXACT)
         return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, kThreads, kThreads, false};
     if (cfg->variant == SLPA_VARIANT_BM)
-        return {k_lane_win<W, BmLane<false>, DET>, k_lane_win<W, BmLane<true>, DET>, k_bm_hi_win<W, DET>, kWinThreads,
-                kWinThreads, true};
-    if (cfg->sketch_slots == 8)
-        return {k_lane_win<W, MgLane<8, false>, DET>, k_lane_win<W, MgLane<8, true>, DET>, k_mg_hi_win<W, 8, DET>,
+        return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
                 kWinThreads, kWinThreads, true};
-    return {k_lane_win<W, MgLane<0, false>, DET>, k_lane_win<W, MgLane<0, true>, DET>, k_mg_hi_win<W, 0, DET>,
-            kWinThreads, kWinThreads, true};
+    if (cfg->sketch_slots == 8)
+        return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
+                k_mg_hi_win<W, 8, DET, V>, kWinThreads, kWinThreads, true};
+    return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
+            k_mg_hi_win<W, 0, DET, V>, kWinThreads, kWinThreads, true};
 }
 
+// Integer sketch values when the exactness precondition holds (slpa_sketch.cuh).
 KernelSet kernels_for(const slpa_ctx *ctx, const slpa_config *cfg, bool det) {
-    if (ctx->g.w_f64) return det ? pick_kernels<double, true>(cfg) : pick_kernels<double, false>(cfg);
-    return det ? pick_kernels<float, true>(cfg) : pick_kernels<float, false>(cfg);
+    static const int force_fp64 = [] {
+        const char *e = getenv("SLPA_FORCE_FP64");
+        return e ? atoi(e) : 0;
+    }();
+    const bool iv = ctx->g.int_weights && !force_fp64;
+    if (ctx->g.w_f64) {
+        if (iv) return det ? pick_kernels<double, true, uint32_t>(cfg) : pick_kernels<double, false, uint32_t>(cfg);
+        return det ? pick_kernels<double, true, double>(cfg) : pick_kernels<double, false, double>(cfg);
+    }
+    if (iv) return det ? pick_kernels<float, true, uint32_t>(cfg) : pick_kernels<float, false, uint32_t>(cfg);
+    return det ? pick_kernels<float, true, double>(cfg) : pick_kernels<float, false, double>(cfg);
 }
 
 SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
@@ -854,6 +880,11 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     a.symmetric = g.symmetric;
     a.thr = cfg->degree_threshold;
     a.single = cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch;
+    static const int dbg = [] {
+        const char *e = getenv("SLPA_DEBUG_SKIP");
+        return e ? atoi(e) : 0;
+    }();
+    a.dbg = dbg;
     return a;
 }
 
@@ -941,14 +972,30 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     const int64_t nwords = (n + 31) / 32;
     unsigned long long *cur_lo = wb.counters.p + CNT_LO * CNT_STRIPES, *cur_mid = wb.counters.p + CNT_MID * CNT_STRIPES,
                        *cur_hi = wb.counters.p + CNT_HI * CNT_STRIPES;
+    // Any fair relaxation order reaches the same (unique) fixpoint, so heavy
+    // vertices may wait: light rounds run until quiet, then one heavy phase.
+    static const int defer = [] {
+        const char *e = getenv("SLPA_DEFER");
+        return e ? atoi(e) : 1;
+    }();
+    bool pend_any = false;
     for (;;) {
         CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_mid, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_hi, 0, sizeof(unsigned long long), s));
-        timed_launch(ctx, SLPA_PROF_COMPACT, (g.n_lo > 0) + (g.n_mid > 0) + (g.n_hi > 0), [&] {
-            launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_a.p, wb.wl_hi.p, cur_hi);
+        timed_launch(ctx, SLPA_PROF_COMPACT, 3, [&] {
             launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
-            launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_a.p, wb.wl_mid.p, cur_mid);
+            if (defer) {
+                if (g.n_hi > 0)
+                    k_defer_dirty<<<grid_for(g.n_hi, kThreads), kThreads, 0, s>>>(g.bin_hi.p, g.n_hi, wb.dirty_a.p,
+                                                                                  wb.dirty_b.p);
+                if (g.n_mid > 0)
+                    k_defer_dirty<<<grid_for(g.n_mid, kThreads), kThreads, 0, s>>>(g.bin_mid.p, g.n_mid,
+                                                                                   wb.dirty_a.p, wb.dirty_b.p);
+            } else {
+                launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_a.p, wb.wl_hi.p, cur_hi);
+                launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_a.p, wb.wl_mid.p, cur_mid);
+            }
             CUDA_TRY(cudaGetLastError());
         });
         CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (size_t)nwords * sizeof(uint32_t), s));
@@ -957,10 +1004,23 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             evals0 = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
             arcs0 = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
             first = false;
+            pend_any = defer != 0;
         }
-        const int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
-                      nhi = (int64_t)ctx->h_sum[CNT_HI];
+        int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
+                nhi = (int64_t)ctx->h_sum[CNT_HI];
+        if (defer && nlo == 0 && pend_any) {  // light vertices quiet: run the pending heavy ones
+            timed_launch(ctx, SLPA_PROF_COMPACT, 2, [&] {
+                launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_b.p, wb.wl_hi.p, cur_hi);
+                launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_b.p, wb.wl_mid.p, cur_mid);
+                CUDA_TRY(cudaGetLastError());
+            });
+            CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+            read_counters(ctx);
+            nmid = (int64_t)ctx->h_sum[CNT_MID];
+            nhi = (int64_t)ctx->h_sum[CNT_HI];
+        }
         if (nlo == 0 && nmid == 0 && nhi == 0) break;
+        pend_any = defer != 0;  // conservatively re-check the pending bitmap once light work drains
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
         launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
         launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
