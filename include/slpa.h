@@ -84,6 +84,7 @@ enum {
     SLPA_PROF_COMPACT = 6,   /* dirty bitmap -> worklists */
     SLPA_PROF_COMMIT = 7,    /* label update, flags, changed-vertex count */
     SLPA_PROF_OTHER = 8,
+    SLPA_PROF_EVAL_GIANT = 9,/* deg >= giant threshold: gather + warp-per-vertex replay (all rounds) */
     SLPA_PROF_N = 12
 };
 typedef struct {

@@ -13,7 +13,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libslpa_b200.so")
+# SLPA_LIB: alternative build of the same ABI (A/B timing experiments only).
+LIB_PATH = os.environ.get("SLPA_LIB") or os.path.join(HERE, "libslpa_b200.so")
 
 SLPA_OK, SLPA_EINVAL, SLPA_ECUDA, SLPA_EUNSUPPORTED, SLPA_ENOGRAPH, SLPA_EHOOK = range(6)
 
@@ -53,7 +54,7 @@ class SlpaRunStats(ctypes.Structure):
 
 PROF_N = 12
 PROF_CLASSES = ("eval_lo_r0", "eval_mid_r0", "eval_hi_r0", "eval_lo_rk", "eval_mid_rk", "eval_hi_rk", "compact",
-                "commit", "other", "unused", "unused", "unused")
+                "commit", "other", "eval_giant", "unused", "unused")
 
 
 class SlpaProfile(ctypes.Structure):

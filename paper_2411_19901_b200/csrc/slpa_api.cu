@@ -44,7 +44,7 @@ void check_gpu_limits(const slpa_ctx *ctx, const slpa_config *cfg) {
     if (cfg->variant == SLPA_VARIANT_MG) {
         SLPA_REQUIRE(cfg->sketch_slots <= SLPA_KDYN, SLPA_EUNSUPPORTED,
                      "sketch_slots > 64 is not supported on the GPU path");
-        if (!cfg->shared_sketch && ctx->g.n_hi > 0)
+        if (!cfg->shared_sketch && ctx->g.n_hi + ctx->g.n_giant > 0)
             SLPA_REQUIRE(cfg->sketch_slots <= SLPA_KHI_MAX, SLPA_EUNSUPPORTED,
                          "sketch_slots > 32 with high-degree vertices is not supported on the GPU path");
     }
@@ -109,6 +109,9 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.wl_lo.alloc(n);
     wb.wl_mid.alloc(n);
     wb.wl_hi.alloc(n);
+    wb.wl_giant.alloc(ctx->g.n_giant + 1);
+    wb.glab.alloc(ctx->g.giant_arcs + 1);
+    wb.gw.alloc((ctx->g.giant_arcs + 1) * (ctx->g.w_f64 ? sizeof(double) : sizeof(float)));
     wb.io_labels.alloc(n);
     wb.io_flags.alloc(n);
     wb.counters.alloc(CNT_TOTAL);
@@ -149,6 +152,9 @@ int32_t slpa_create(int32_t device, slpa_ctx **out) {
             CUDA_TRY(cudaEventCreate(&c->ev1));
             CUDA_TRY(cudaEventCreate(&c->pev0));
             CUDA_TRY(cudaEventCreate(&c->pev1));
+            CUDA_TRY(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming));
         } catch (...) {
             delete c;
             throw;
@@ -171,9 +177,12 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     ctx->g.bin_lo.release();
     ctx->g.bin_mid.release();
     ctx->g.bin_hi.release();
+    ctx->g.bin_giant.release();
+    ctx->g.giant_off.release();
     WorkBuffers &wb = ctx->wb;
     wb.lab_old.release(); wb.lab_new.release(); wb.flag_a.release(); wb.flag_b.release();
-    wb.dirty_a.release(); wb.dirty_b.release(); wb.wl_lo.release(); wb.wl_mid.release(); wb.wl_hi.release();
+    wb.dirty_a.release(); wb.dirty_b.release(); wb.wl_lo.release(); wb.wl_mid.release(); wb.wl_hi.release(); wb.wl_giant.release();
+    wb.glab.release(); wb.gw.release();
     wb.io_labels.release(); wb.io_flags.release(); wb.counters.release(); wb.metric_d.release();
     wb.metric_u.release(); wb.scratch.release();
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -181,6 +190,12 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->pev0) cudaEventDestroy(ctx->pev0);
     if (ctx->pev1) cudaEventDestroy(ctx->pev1);
+    if (ctx->gev0) cudaEventDestroy(ctx->gev0);
+    if (ctx->gev1) cudaEventDestroy(ctx->gev1);
+    if (ctx->stream2) {
+        cudaStreamSynchronize(ctx->stream2);
+        cudaStreamDestroy(ctx->stream2);
+    }
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return SLPA_OK;

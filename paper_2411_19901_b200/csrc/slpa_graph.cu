@@ -149,12 +149,13 @@ __global__ void k_perm_rows(const int64_t *off, const int32_t *tgt, const W *w, 
 }
 
 // ------------------------------------------------------------------ bins
-__global__ void k_classify(const int64_t *off, int64_t n, int32_t thr, int32_t hsplit, int32_t single,
-                           uint8_t *cls) {
+__global__ void k_classify(const int64_t *off, int64_t n, int32_t thr, int32_t hsplit, int32_t gsplit,
+                           int32_t single, uint8_t *cls) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     int64_t d = off[v + 1] - off[v];
-    cls[v] = d == 0 ? CLS_NONE : ((single || d < thr) ? CLS_LO : (d < hsplit ? CLS_MID : CLS_HI));
+    cls[v] = d == 0 ? CLS_NONE
+                    : ((single || d < thr) ? CLS_LO : (d < hsplit ? CLS_MID : (d < gsplit ? CLS_HI : CLS_GIANT)));
 }
 struct IsClass {
     const uint8_t *cls;
@@ -535,6 +536,14 @@ void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order, bool on_device)
     slpa_graph_finalize(ctx);
 }
 
+static int64_t giant_split() {
+    static int64_t v = [] {
+        const char *e = getenv("SLPA_GIANT");
+        return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)65536;
+    }();
+    return v;
+}
+
 static int64_t hi_split() {
     static int64_t v = [] {
         const char *e = getenv("SLPA_HI_SPLIT");
@@ -568,15 +577,19 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
     // mid = D_H <= deg < max(D_H, hi_split) (one lane, R_H chunks),
     // hi = the rest (one warp, lane = chunk).
     const int64_t hs = std::max<int64_t>(cfg->degree_threshold, hi_split());
+    const int64_t gs = std::max<int64_t>(hs, giant_split());
     const int32_t hsplit = (int32_t)std::min<int64_t>(hs, INT32_MAX);
-    if (n > 0) k_classify<<<grid_for(n, kT), kT, 0, s>>>(g.off(), n, cfg->degree_threshold, hsplit, single, g.cls.p);
+    const int32_t gsplit = (int32_t)std::min<int64_t>(gs, INT32_MAX);
+    g.bin_giant.alloc(n);
+    if (n > 0)
+        k_classify<<<grid_for(n, kT), kT, 0, s>>>(g.off(), n, cfg->degree_threshold, hsplit, gsplit, single, g.cls.p);
     CUDA_TRY(cudaGetLastError());
     DevBuf<int64_t> cnt;
-    cnt.alloc(3);
+    cnt.alloc(4);
     cub::CountingInputIterator<int32_t> it(0);
-    const uint8_t classes[3] = {CLS_LO, CLS_MID, CLS_HI};
-    int32_t *outs[3] = {g.bin_lo.p, g.bin_mid.p, g.bin_hi.p};
-    for (int which = 0; which < 3; ++which) {
+    const uint8_t classes[4] = {CLS_LO, CLS_MID, CLS_HI, CLS_GIANT};
+    int32_t *outs[4] = {g.bin_lo.p, g.bin_mid.p, g.bin_hi.p, g.bin_giant.p};
+    for (int which = 0; which < 4; ++which) {
         IsClass pred{g.cls.p, classes[which]};
         int32_t *out = outs[which];
         int64_t *nsel = cnt.p + which;
@@ -584,16 +597,18 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
             return cub::DeviceSelect::If(tmp, bytes, it, out, nsel, n, pred, s);
         });
     }
-    int64_t h[3] = {0, 0, 0};
+    int64_t h[4] = {0, 0, 0, 0};
     CUDA_TRY(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     g.n_lo = h[0];
     g.n_mid = h[1];
     g.n_hi = h[2];
-    // hi: descending degree (longest scans first); lo / mid: ascending
-    // degree, stable on position (degree-homogeneous warps)
-    for (int which = 0; which < 3; ++which) {
-        const int64_t cntb = which == 2 ? g.n_hi : (which == 1 ? g.n_mid : (lo_sorted ? g.n_lo : 0));
+    g.n_giant = h[3];
+    // hi / giant: descending degree (longest scans first); lo / mid:
+    // ascending degree, stable on position (degree-homogeneous warps)
+    for (int which = 0; which < 4; ++which) {
+        const int64_t cntb = which >= 2 ? (which == 2 ? g.n_hi : g.n_giant)
+                                        : (which == 1 ? g.n_mid : (lo_sorted ? g.n_lo : 0));
         int32_t *binp = outs[which];
         if (cntb <= 1) continue;
         DevBuf<int64_t> dk, dk2;
@@ -605,7 +620,7 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
         int64_t *k1 = dk.p, *k2 = dk2.p;
         int32_t *v1 = binp, *vv2 = v2.p;
         const int64_t nh = cntb;
-        if (which == 2)
+        if (which >= 2)
             cub_call(ctx, [&](void *tmp, size_t &bytes) {
                 return cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k1, k2, v1, vv2, nh, 0, 40, s);
             });
@@ -615,6 +630,21 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
             });
         CUDA_TRY(cudaMemcpyAsync(binp, v2.p, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    // giant gather-buffer offsets: exclusive prefix of the giants' degrees
+    g.giant_off.alloc(g.n_giant + 1);
+    g.giant_arcs = 0;
+    if (g.n_giant > 0) {
+        DevBuf<int64_t> dk;
+        dk.alloc(g.n_giant + 1);
+        CUDA_TRY(cudaMemsetAsync(dk.p, 0, (g.n_giant + 1) * sizeof(int64_t), s));
+        k_bin_degrees<<<grid_for(g.n_giant, kT), kT, 0, s>>>(g.off(), g.bin_giant.p, g.n_giant, dk.p);
+        int64_t *din = dk.p, *dout = g.giant_off.p;
+        const int64_t nn = g.n_giant + 1;
+        cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceScan::ExclusiveSum(tmp, bytes, din, dout, nn, s); });
+        CUDA_TRY(cudaMemcpyAsync(&g.giant_arcs, g.giant_off.p + g.n_giant, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        dk.release();
     }
     g.bin_thr = cfg->degree_threshold;
     g.bin_single = single;

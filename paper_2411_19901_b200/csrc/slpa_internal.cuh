@@ -23,7 +23,7 @@
 #define SLPA_KDYN 64          // max sketch slots on the dynamic-k path
 #define SLPA_KHI_MAX 32       // slot-parallel merge holds one slot per lane
 
-enum { CLS_NONE = 0, CLS_LO = 1, CLS_HI = 2, CLS_MID = 3 };
+enum { CLS_NONE = 0, CLS_LO = 1, CLS_HI = 2, CLS_MID = 3, CLS_GIANT = 4 };
 
 struct SlpaError {
     int32_t code;
@@ -83,9 +83,13 @@ struct SweepArgs {
     int32_t thr;                      // degree_threshold (chunked evaluation at deg >= thr)
     int32_t single;                   // shared_sketch: one sketch over any degree
     int32_t dbg;                      // timing experiments only (SLPA_DEBUG_SKIP); 0 in production
+    const int32_t *giant_bin;         // giant vertices (deg >= giant threshold), degree desc
+    const int64_t *giant_off;         // exclusive prefix of their degrees
+    uint32_t *glab;                   // gathered label words of their arcs
+    void *gw;                         // gathered weights (W)
 };
 
-enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_N = 8 };
+enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_GIANT = 8, CNT_N = 9 };
 #define CNT_STRIPES 64
 #define CNT_TOTAL (CNT_N * CNT_STRIPES)
 
@@ -116,15 +120,16 @@ struct DeviceGraph {
     int32_t bin_single = -1;  // all non-empty vertices in the low bin (exact / shared sketch)
     int32_t bin_lo_sorted = -1;
     DevBuf<uint8_t> cls;
-    DevBuf<int32_t> bin_lo, bin_mid, bin_hi;
-    int64_t n_lo = 0, n_mid = 0, n_hi = 0;
+    DevBuf<int32_t> bin_lo, bin_mid, bin_hi, bin_giant;
+    DevBuf<int64_t> giant_off;  // exclusive prefix of giant degrees (n_giant + 1)
+    int64_t n_lo = 0, n_mid = 0, n_hi = 0, n_giant = 0, giant_arcs = 0;
     const Csr &act() const { return has_order ? perm : base; }
     const int64_t *off() const { return act().off.p; }
     const int32_t *tgt() const { return act().tgt.p; }
     const void *w() const { return w_f64 ? (const void *)act().w64.p : (const void *)act().w32.p; }
     size_t bytes() const {
         return base.bytes() + perm.bytes() + ids.bytes() + pos.bytes() + roff.bytes() + rsrc.bytes() + cls.bytes() +
-               bin_lo.bytes() + bin_mid.bytes() + bin_hi.bytes();
+               bin_lo.bytes() + bin_mid.bytes() + bin_hi.bytes() + bin_giant.bytes() + giant_off.bytes();
     }
     size_t csr_bytes() const { return act().bytes(); }
 };
@@ -134,7 +139,9 @@ struct WorkBuffers {
     DevBuf<uint32_t> lab_new;
     DevBuf<uint8_t> flag_a, flag_b;
     DevBuf<uint32_t> dirty_a, dirty_b;
-    DevBuf<int32_t> wl_lo, wl_mid, wl_hi;
+    DevBuf<int32_t> wl_lo, wl_mid, wl_hi, wl_giant;
+    DevBuf<uint32_t> glab;        // giant gather buffers
+    DevBuf<unsigned char> gw;
     DevBuf<int32_t> io_labels;  // staging for host <-> device label exchange
     DevBuf<uint8_t> io_flags;
     DevBuf<unsigned long long> counters;
@@ -143,7 +150,7 @@ struct WorkBuffers {
     DevBuf<unsigned char> scratch;  // cub temp storage
     size_t bytes() const {
         return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() +
-               dirty_b.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + io_labels.bytes() + io_flags.bytes() +
+               dirty_b.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
     }
 };
@@ -161,6 +168,9 @@ struct slpa_ctx {
     int32_t prof_on = 0;
     slpa_profile prof{};
     cudaEvent_t pev0 = nullptr, pev1 = nullptr;
+    cudaStream_t stream2 = nullptr;          // giant-vertex work overlapping the main stream
+    cudaEvent_t gev0 = nullptr, gev1 = nullptr;
+    int32_t giant_pending = 0;
     int32_t have_labels = 0;   // lab_old holds labels of a finished run
     // multi-GPU partition
     int32_t part = 0;

@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wid >= count) return;  // warp-uniform
+    if (((a.dbg & 4) && wid != 0) || ((a.dbg & 8) && wid == 0)) return;  // timing experiments only
     const int32_t v = __ldg(&list[wid]);
     const uint8_t f0 = a.flag_cur[v];
     if (DET) {
@@ -628,6 +629,219 @@ __global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const in
     warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
 }
 
+// ================================================================== giant vertices
+// deg >= giant threshold: a single warp per vertex would walk deg/32 arcs per
+// lane with dependent staging latencies on every window -- the tail of every
+// heavy phase (8 ms for the 406k-degree hub at RMAT s24).  Two kernels:
+//  (A) gather: a block per giant materialises its arcs' (label word, weight)
+//      stream -- lower neighbours' L1|changed, higher neighbours' L0, self
+//      arcs weight 0 -- coalesced and fully parallel;
+//  (B) scan: a warp per giant, lane g replays chunk g from that contiguous
+//      buffer with register double-buffered prefetch, so the per-lane chain
+//      runs at ALU speed; then the ordered merge as in k_mg_hi_win.
+constexpr int kGatherThreads = 256;
+
+template <class W, bool DET>
+__global__ void __launch_bounds__(kGatherThreads) k_giant_gather(SweepArgs a, const int32_t *__restrict__ slots,
+                                                                 int64_t count, int round0) {
+    const int64_t b = blockIdx.x;
+    if (b >= count) return;
+    const int32_t slot = __ldg(&slots[b]);
+    const int32_t v = __ldg(&a.giant_bin[slot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET ? (round0 && !f0) : !f0) return;
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    W *gw = reinterpret_cast<W *>(a.gw);
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t base = __ldg(&a.giant_off[slot]) - lo;
+    const uint64_t pol = policy_evict_first();
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        const int32_t t = ld_stream(&a.tgt[e], pol);
+        W w = ld_stream(&wts[e], pol);
+        uint32_t L = 0;
+        if (t == v) {
+            w = (W)0;
+        } else if (DET) {
+            L = __ldcg(&a.lab_new[t]);
+            if (t > v && (L >> 31)) L = (uint32_t)__ldg(&a.lab_old[t]);
+        } else {
+            L = (uint32_t)__ldcg(&a.lab_old[t]);
+        }
+        a.glab[base + e] = L;
+        gw[base + e] = w;
+    }
+}
+
+// Per-lane replay of [x, end) of a giant's gathered stream, 16-element
+// register batches, next batch loaded before the current one is consumed.
+template <class W, class F>
+__device__ __forceinline__ void giant_stream(const SweepArgs &a, int64_t x, int64_t end, bool &lower_changed, F &&f) {
+    constexpr int B = 16;
+    const W *gw = reinterpret_cast<const W *>(a.gw);
+    uint32_t La[B], Lb[B];
+    W wa[B], wb[B];
+    auto load = [&](uint32_t (&L)[B], W (&w)[B], int64_t p) {
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (p + j < end) {
+                L[j] = __ldcg(&a.glab[p + j]);
+                w[j] = __ldcg(&gw[p + j]);
+            } else {
+                L[j] = 0;
+                w[j] = (W)0;
+            }
+        }
+    };
+    auto use = [&](const uint32_t (&L)[B], const W (&w)[B]) {
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (w[j] != (W)0) {
+                lower_changed |= (L[j] >> 31) != 0;
+                f((int32_t)(L[j] & SLPA_LMASK), w[j]);
+            }
+        }
+    };
+    if (x >= end) return;
+    load(La, wa, x);
+    for (;;) {
+        const int64_t nx = x + B;
+        if (nx < end) load(Lb, wb, nx);
+        use(La, wa);
+        if (nx >= end) break;
+        x = nx + B;
+        if (x < end) load(La, wa, x);
+        use(Lb, wb);
+        if (x >= end) break;
+    }
+}
+
+template <class W, int K, bool DET, class V>
+__global__ void __launch_bounds__(kWinThreads) k_mg_giant(SweepArgs a, const int32_t *__restrict__ slots,
+                                                          int64_t count, int round0) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t slot = __ldg(&slots[wid]);
+    const int32_t v = __ldg(&a.giant_bin[slot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int64_t base = __ldg(&a.giant_off[slot]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int k = K > 0 ? K : a.k;
+    const int P = a.parts;
+    bool lower_changed = false;
+    WarpSketch<V> S_{0, (V)0};
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        MgSketchDev<K, V> part;
+        part.reset(k);
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
+        giant_stream<W>(a, base + cs, base + ce, lower_changed, [&](int32_t c, W w) { part.acc(c, (V)w, k); });
+        int first = 0;
+        if (b0 == 0) {
+#pragma unroll
+            for (int i = 0; i < KArr<K>::v; ++i) {
+                if (K == 0 && i >= k) break;
+                int32_t kk = __shfl_sync(0xffffffffu, part.key[i], 0);
+                V vv = __shfl_sync(0xffffffffu, part.val[i], 0);
+                if (lane == i) { S_.key = kk; S_.val = vv; }
+            }
+            first = 1;
+        }
+        const int nb = min(32, P - b0);
+        unsigned nz = 0;
+#pragma unroll
+        for (int i = 0; i < KArr<K>::v; ++i) {
+            if (K == 0 && i >= k) break;
+            if (part.val[i] > (V)0) nz |= 1u << (i & 31);
+        }
+        for (int q = first; q < nb; ++q) {
+            const unsigned mq = __shfl_sync(0xffffffffu, nz, q);
+            if (!mq) continue;
+#pragma unroll
+            for (int i = 0; i < KArr<K>::v; ++i) {
+                if (K == 0 && i >= k) break;
+                if (!(mq & (1u << (i & 31)))) continue;
+                int32_t c = __shfl_sync(0xffffffffu, part.key[i], q);
+                V w = __shfl_sync(0xffffffffu, part.val[i], q);
+                S_.acc(lane, k, c, w);
+            }
+        }
+    }
+    if (a.scan_double) {  // exact per-key re-count in adjacency order, from the gathered stream
+        S_.val = (V)0;
+        const W *gw = reinterpret_cast<const W *>(a.gw);
+        for (int64_t b = 0; b < deg; b += 32) {
+            const int64_t x = b + lane;
+            int32_t c = 0;
+            V w = (V)0;
+            if (x < deg) {
+                w = (V)__ldcg(&gw[base + x]);
+                c = (int32_t)(__ldcg(&a.glab[base + x]) & SLPA_LMASK);
+            }
+            unsigned okm = __ballot_sync(0xffffffffu, w != (V)0);
+            while (okm) {
+                int j = __ffs(okm) - 1;
+                okm &= okm - 1;
+                S_.rescan_add(lane, k, __shfl_sync(0xffffffffu, c, j), __shfl_sync(0xffffffffu, w, j));
+            }
+        }
+    }
+    int32_t best;
+    const bool found = S_.max_key(lane, k, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
+}
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kWinThreads) k_bm_giant(SweepArgs a, const int32_t *__restrict__ slots,
+                                                          int64_t count, int round0) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t slot = __ldg(&slots[wid]);
+    const int32_t v = __ldg(&a.giant_bin[slot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int64_t base = __ldg(&a.giant_off[slot]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int P = a.parts;
+    bool lower_changed = false, have = false;
+    int32_t bc = 0;
+    V bw = (V)0;
+    for (int p = lane; p < P; p += 32) {
+        int64_t cs, ce;
+        chunk_bounds(deg, P, p, cs, ce);
+        BmVote<V> st{cur, (V)0};
+        giant_stream<W>(a, base + cs, base + ce, lower_changed, [&](int32_t c, W w) { st.acc(c, (V)w); });
+        if (!have || bm_better(st.w, st.cand, bw, bc)) { bc = st.cand; bw = st.w; have = true; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+        int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        V ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
+    }
+    warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
+}
+
 // ================================================================== exact
 // select_label_exact (lpa.py:92-107): per-label totals summed in adjacency
 // order (np.bincount order), argmax = smallest label among ties.  One thread
@@ -688,6 +902,17 @@ __global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *
 }
 
 // ================================================================== round plumbing
+// Round 0 with heavy vertices deferred from the start: flagged heavy
+// vertices go straight to the pending bitmap.
+__global__ void __launch_bounds__(kThreads) k_defer_flagged(const int32_t *__restrict__ bin, int64_t count,
+                                                            const uint8_t *__restrict__ flags,
+                                                            uint32_t *__restrict__ pend) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int32_t v = __ldg(&bin[i]);
+    if (flags[v]) atomicOr(&pend[v >> 5], 1u << (v & 31));
+}
+
 // Deferred heavy (mid / hi) vertices: their dirty bits move to a persistent
 // pending bitmap and are only re-evaluated once the light vertices are quiet.
 __global__ void __launch_bounds__(kThreads) k_defer_dirty(const int32_t *__restrict__ bin, int64_t count,
@@ -706,7 +931,7 @@ __global__ void __launch_bounds__(kThreads) k_defer_dirty(const int32_t *__restr
 __global__ void __launch_bounds__(kThreads) k_filter_dirty(const int32_t *__restrict__ bin, int64_t count,
                                                            const uint32_t *__restrict__ dirty,
                                                            int32_t *__restrict__ out,
-                                                           unsigned long long *__restrict__ cursor) {
+                                                           unsigned long long *__restrict__ cursor, int as_index) {
     __shared__ int s_warp[kThreads / 32];
     __shared__ unsigned long long s_base;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -730,7 +955,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_dirty(const int32_t *__rest
         s_base = tot ? atomicAdd(cursor, (unsigned long long)tot) : 0ull;
     }
     __syncthreads();
-    if (hit) out[s_base + s_warp[w] + __popc(m & ((1u << lane) - 1))] = v;
+    if (hit) out[s_base + s_warp[w] + __popc(m & ((1u << lane) - 1))] = as_index ? (int32_t)i : v;
 }
 
 // End of a deterministic sweep: fold L1 into L0, count ΔN, and set the
@@ -822,9 +1047,10 @@ __global__ void k_sync_lab_new(const int32_t *lab_old, uint32_t *lab_new, int64_
 typedef void (*EvalKernel)(SweepArgs, const int32_t *, int64_t, int);
 
 // lo: one lane per vertex, one sketch; mid: one lane per vertex, R_H chunks;
-// hi: one warp per vertex, lane = chunk (or thread-per-vertex for `exact`).
+// hi: one warp per vertex, lane = chunk (or thread-per-vertex for `exact`);
+// giant: gather + warp-per-vertex replay.
 struct KernelSet {
-    EvalKernel lo, mid, hi;
+    EvalKernel lo, mid, hi, gather, giant;
     int lo_threads, hi_threads;
     bool hi_is_warp;
 };
@@ -832,15 +1058,17 @@ struct KernelSet {
 template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
     if (cfg->variant == SLPA_VARIANT_EXACT)
-        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, kThreads, kThreads, false};
+        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, false};
     if (cfg->variant == SLPA_VARIANT_BM)
         return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
-                kWinThreads, kWinThreads, true};
+                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, true};
     if (cfg->sketch_slots == 8)
         return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
-                k_mg_hi_win<W, 8, DET, V>, kWinThreads, kWinThreads, true};
+                k_mg_hi_win<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kWinThreads,
+                kWinThreads, true};
     return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
-            k_mg_hi_win<W, 0, DET, V>, kWinThreads, kWinThreads, true};
+            k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads, kWinThreads,
+            true};
 }
 
 // Integer sketch values when the exactness precondition holds (slpa_sketch.cuh).
@@ -885,6 +1113,10 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         return e ? atoi(e) : 0;
     }();
     a.dbg = dbg;
+    a.giant_bin = g.bin_giant.p;
+    a.giant_off = g.giant_off.p;
+    a.glab = ctx->wb.glab.p;
+    a.gw = ctx->wb.gw.p;
     return a;
 }
 
@@ -943,10 +1175,45 @@ void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int
     });
 }
 
+// Giants: gather then replay; `slots` index bin_giant.  They are a handful
+// of warps, so (outside profiling) they run on a second stream, overlapping
+// the other kernels of the round; giant_join() makes the main stream wait.
+void launch_giant(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int32_t *slots, int64_t cnt,
+                  int round0) {
+    if (cnt <= 0 || !ks.gather) return;
+    const bool overlap = !ctx->prof_on;
+    cudaStream_t gs = overlap ? ctx->stream2 : ctx->stream;
+    if (overlap) {
+        CUDA_TRY(cudaEventRecord(ctx->gev0, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(gs, ctx->gev0, 0));
+    }
+    timed_launch(ctx, SLPA_PROF_EVAL_GIANT, 2, [&] {
+        ks.gather<<<(unsigned)cnt, kGatherThreads, 0, gs>>>(a, slots, cnt, round0);
+        ks.giant<<<grid_for(cnt * 32, kWinThreads), kWinThreads, 0, gs>>>(a, slots, cnt, round0);
+        CUDA_TRY(cudaGetLastError());
+    });
+    if (overlap) {
+        CUDA_TRY(cudaEventRecord(ctx->gev1, gs));
+        ctx->giant_pending = 1;
+    }
+}
+
+void giant_join(slpa_ctx *ctx) {
+    if (ctx->giant_pending) {
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->gev1, 0));
+        ctx->giant_pending = 0;
+    }
+}
+
 void launch_filter(cudaStream_t s, const int32_t *bin, int64_t count, const uint32_t *dirty, int32_t *out,
-                   unsigned long long *cursor) {
+                   unsigned long long *cursor, int as_index = 0) {
     if (count <= 0) return;
-    k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor);
+    k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor, as_index);
+}
+
+__global__ void k_iota(int32_t *out, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)i;
 }
 
 }  // namespace
@@ -962,39 +1229,57 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(wb.flag_b.p, 0, (size_t)n, s));
     for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
-    // round 0: every flagged vertex, straight from the degree bins
-    launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+    static const int defer = [] {
+        const char *e = getenv("SLPA_DEFER");
+        return e ? atoi(e) : 2;
+    }();
+    const int64_t nwords = (n + 31) / 32;
+    // round 0: every flagged vertex, straight from the degree bins.  With
+    // defer >= 2 the heavy ones (mid / hi / giant) wait for the light ones
+    // to settle first -- any fair order reaches the same unique fixpoint.
+    if (defer >= 2) {
+        const int32_t *heavy[3] = {g.bin_hi.p, g.bin_mid.p, g.bin_giant.p};
+        const int64_t nheavy[3] = {g.n_hi, g.n_mid, g.n_giant};
+        for (int h = 0; h < 3; ++h)
+            if (nheavy[h] > 0)
+                k_defer_flagged<<<grid_for(nheavy[h], kThreads), kThreads, 0, s>>>(heavy[h], nheavy[h], wb.flag_a.p,
+                                                                                  wb.dirty_b.p);
+        CUDA_TRY(cudaGetLastError());
+    } else {
+        if (g.n_giant > 0) {
+            k_iota<<<grid_for(g.n_giant, kThreads), kThreads, 0, s>>>(wb.wl_giant.p, g.n_giant);
+            launch_giant(ctx, ks, a, wb.wl_giant.p, g.n_giant, 1);
+        }
+        launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+        launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
+    }
     launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
-    launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
     int64_t rounds = 1;
     unsigned long long evals0 = 0, arcs0 = 0;
     bool first = true;
-    const int64_t nwords = (n + 31) / 32;
     unsigned long long *cur_lo = wb.counters.p + CNT_LO * CNT_STRIPES, *cur_mid = wb.counters.p + CNT_MID * CNT_STRIPES,
-                       *cur_hi = wb.counters.p + CNT_HI * CNT_STRIPES;
-    // Any fair relaxation order reaches the same (unique) fixpoint, so heavy
-    // vertices may wait: light rounds run until quiet, then one heavy phase.
-    static const int defer = [] {
-        const char *e = getenv("SLPA_DEFER");
-        return e ? atoi(e) : 1;
-    }();
-    bool pend_any = false;
+                       *cur_hi = wb.counters.p + CNT_HI * CNT_STRIPES,
+                       *cur_giant = wb.counters.p + CNT_GIANT * CNT_STRIPES;
+    bool pend_any = defer != 0;
     for (;;) {
+        giant_join(ctx);
         CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_mid, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_hi, 0, sizeof(unsigned long long), s));
-        timed_launch(ctx, SLPA_PROF_COMPACT, 3, [&] {
+        CUDA_TRY(cudaMemsetAsync(cur_giant, 0, sizeof(unsigned long long), s));
+        timed_launch(ctx, SLPA_PROF_COMPACT, 4, [&] {
             launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
             if (defer) {
-                if (g.n_hi > 0)
-                    k_defer_dirty<<<grid_for(g.n_hi, kThreads), kThreads, 0, s>>>(g.bin_hi.p, g.n_hi, wb.dirty_a.p,
-                                                                                  wb.dirty_b.p);
-                if (g.n_mid > 0)
-                    k_defer_dirty<<<grid_for(g.n_mid, kThreads), kThreads, 0, s>>>(g.bin_mid.p, g.n_mid,
-                                                                                   wb.dirty_a.p, wb.dirty_b.p);
+                const int32_t *heavy[3] = {g.bin_hi.p, g.bin_mid.p, g.bin_giant.p};
+                const int64_t nheavy[3] = {g.n_hi, g.n_mid, g.n_giant};
+                for (int h = 0; h < 3; ++h)
+                    if (nheavy[h] > 0)
+                        k_defer_dirty<<<grid_for(nheavy[h], kThreads), kThreads, 0, s>>>(heavy[h], nheavy[h],
+                                                                                        wb.dirty_a.p, wb.dirty_b.p);
             } else {
                 launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_a.p, wb.wl_hi.p, cur_hi);
                 launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_a.p, wb.wl_mid.p, cur_mid);
+                launch_filter(s, g.bin_giant.p, g.n_giant, wb.dirty_a.p, wb.wl_giant.p, cur_giant, 1);
             }
             CUDA_TRY(cudaGetLastError());
         });
@@ -1004,35 +1289,40 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             evals0 = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
             arcs0 = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
             first = false;
-            pend_any = defer != 0;
         }
         int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
-                nhi = (int64_t)ctx->h_sum[CNT_HI];
+                nhi = (int64_t)ctx->h_sum[CNT_HI], ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
         if (defer && nlo == 0 && pend_any) {  // light vertices quiet: run the pending heavy ones
-            timed_launch(ctx, SLPA_PROF_COMPACT, 2, [&] {
+            timed_launch(ctx, SLPA_PROF_COMPACT, 3, [&] {
                 launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_b.p, wb.wl_hi.p, cur_hi);
                 launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_b.p, wb.wl_mid.p, cur_mid);
+                launch_filter(s, g.bin_giant.p, g.n_giant, wb.dirty_b.p, wb.wl_giant.p, cur_giant, 1);
                 CUDA_TRY(cudaGetLastError());
             });
             CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (size_t)nwords * sizeof(uint32_t), s));
             read_counters(ctx);
             nmid = (int64_t)ctx->h_sum[CNT_MID];
             nhi = (int64_t)ctx->h_sum[CNT_HI];
+            ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
         }
-        if (nlo == 0 && nmid == 0 && nhi == 0) break;
-        pend_any = defer != 0;  // conservatively re-check the pending bitmap once light work drains
+        if (nlo == 0 && nmid == 0 && nhi == 0 && ngiant == 0) break;
+        pend_any = defer != 0;
+        launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
         launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
         launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
         ++rounds;
     }
+    giant_join(ctx);
     const unsigned long long evals = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
     const unsigned long long arcs = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
     // commit: L0 <- L1, delta, next-sweep flags
-    timed_launch(ctx, SLPA_PROF_COMMIT, (g.n_lo > 0) + (g.n_mid > 0) + (g.n_hi > 0), [&] {
+    timed_launch(ctx, SLPA_PROF_COMMIT, 4, [&] {
         if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
         if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
         if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
+        if (g.n_giant > 0)
+            k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
         CUDA_TRY(cudaGetLastError());
     });
     read_counters(ctx);
@@ -1054,9 +1344,14 @@ int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
     for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
     // Higher-degree vertices first: they carry most arcs and the tail.
+    if (g.n_giant > 0) {
+        k_iota<<<grid_for(g.n_giant, kThreads), kThreads, 0, s>>>(wb.wl_giant.p, g.n_giant);
+        launch_giant(ctx, ks, a, wb.wl_giant.p, g.n_giant, 1);
+    }
     launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
     launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
     launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    giant_join(ctx);
     if (!ctx->part) {  // partitioned: remote entries hold outgoing marks, cleared after the exchange
         timed_launch(ctx, SLPA_PROF_OTHER, 1, [&] {
             k_clear_isolated_flags<<<grid_for(g.n, kThreads), kThreads, 0, s>>>(wb.flag_a.p, g.cls.p, g.n);
