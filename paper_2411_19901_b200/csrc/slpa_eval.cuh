@@ -1,0 +1,1351 @@
+// slpa_eval.cuh -- the vertex-evaluation kernels of a sweep (templates only;
+// instantiated per weight type / sketch value type / mode in slpa_eval_*.cu so
+// the heavy template code compiles in parallel translation units).
+#pragma once
+#include <cstdlib>
+#include "slpa_sketch.cuh"
+#include "slpa_internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ label reads
+// Deterministic mode: neighbour t of v (positions).  Lower neighbours give
+// L1 (speculative, possibly written this round -> L2 load), higher ones L0.
+// The hot array is lab_new (L1 | changed<<31); a higher neighbour's L0 is
+// fetched from lab_old only when its changed bit is set, so most gathers
+// touch one n*4-byte array (L2-resident at RMAT scale 24).
+__device__ __forceinline__ int32_t det_label(const SweepArgs &a, int32_t t, int32_t v, bool &lower_changed) {
+    const uint32_t L = __ldcg(&a.lab_new[t]);
+    if (t < v) {
+        lower_changed |= (L >> 31) != 0;
+        return (int32_t)(L & SLPA_LMASK);
+    }
+    return (L >> 31) ? __ldg(&a.lab_old[t]) : (int32_t)L;
+}
+
+__device__ __forceinline__ int32_t async_label(const SweepArgs &a, int32_t t) { return __ldcg(&a.lab_old[t]); }
+
+// CSR streams (read once per sweep) are loaded with an L2 evict-first policy
+// so they do not push the label array out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *ptr, uint64_t pol) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float ld_stream(const float *ptr, uint64_t pol) {
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_stream(const double *ptr, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
+template <class W>
+__device__ __forceinline__ double arc_weight(const SweepArgs &a, int64_t e) {
+    return (double)__ldg(reinterpret_cast<const W *>(a.w) + e);
+}
+
+// T for an asymmetric graph: some lower in-neighbour changed.
+__device__ __forceinline__ bool lower_in_changed(const SweepArgs &a, int32_t v) {
+    for (int64_t e = a.roff[v]; e < a.roff[v + 1]; ++e) {
+        int32_t u = a.rsrc[e];
+        if (u < v && (__ldcg(&a.lab_new[u]) >> 31)) return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ void mark_dirty(uint32_t *bm, int32_t t) { atomicOr(&bm[t >> 5], 1u << (t & 31)); }
+
+// Re-queue v's higher-positioned dependants (readers of v's label and
+// vertices whose turn depends on v's changed bit).
+__device__ __forceinline__ void mark_dependants(const SweepArgs &a, int32_t v, int64_t lo, int64_t hi, int start,
+                                                int stride) {
+    for (int64_t e = lo + start; e < hi; e += stride) {
+        int32_t t = __ldg(&a.tgt[e]);
+        if (t > v) mark_dirty(a.dirty_next, t);
+    }
+    if (!a.symmetric) {
+        for (int64_t e = a.roff[v] + start; e < a.roff[v + 1]; e += stride) {
+            int32_t u = a.rsrc[e];
+            if (u > v) mark_dirty(a.dirty_next, u);
+        }
+    }
+}
+
+// Counters are striped over CNT_STRIPES slots (by warp) so that per-warp
+// atomics do not serialise on one L2 address; the host sums the stripes.
+__device__ __forceinline__ int stripe() {
+    return (int)((((unsigned)blockIdx.x * blockDim.x + threadIdx.x) >> 5) & (CNT_STRIPES - 1));
+}
+__device__ __forceinline__ void ctr_add(unsigned long long *ctr, int which, unsigned long long x) {
+    atomicAdd(&ctr[which * CNT_STRIPES + stripe()], x);
+}
+
+// Warp-aggregated counter update; every lane of the warp must call it.
+__device__ __forceinline__ void warp_count(unsigned long long *ctr, unsigned long long evals,
+                                           unsigned long long arcs, unsigned long long delta) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        evals += __shfl_xor_sync(0xffffffffu, evals, o);
+        arcs += __shfl_xor_sync(0xffffffffu, arcs, o);
+        delta += __shfl_xor_sync(0xffffffffu, delta, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        const int s = stripe();
+        if (evals) atomicAdd(&ctr[CNT_EVALS * CNT_STRIPES + s], evals);
+        if (arcs) atomicAdd(&ctr[CNT_ARCS * CNT_STRIPES + s], arcs);
+        if (delta) atomicAdd(&ctr[CNT_DELTA * CNT_STRIPES + s], delta);
+    }
+}
+
+// Finish one deterministic evaluation (thread-per-vertex flavour).
+__device__ __forceinline__ void det_commit_output(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand, bool T,
+                                                  int64_t lo, int64_t hi) {
+    bool chg = T && cand != cur && (!a.pickless || cand < cur);
+    uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
+    uint32_t ow = __ldcg(&a.lab_new[v]);
+    if (nw != ow) {
+        __stcg(&a.lab_new[v], nw);
+        mark_dependants(a, v, lo, hi, 0, 1);
+    }
+}
+
+__device__ __forceinline__ void async_commit_output(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand,
+                                                    int64_t lo, int64_t hi, unsigned long long &delta) {
+    if (cand != cur && (!a.pickless || cand < cur)) {
+        __stcg(&a.lab_old[v], cand);
+        delta = 1;
+        for (int64_t e = lo; e < hi; ++e) a.flag_cur[__ldg(&a.tgt[e])] = 1;
+    }
+}
+
+// Finish one evaluation in a warp-per-vertex kernel (all lanes call it with
+// warp-uniform arguments except lower_changed).
+template <bool DET>
+__device__ __forceinline__ void warp_hi_finish(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand, uint8_t f0,
+                                               bool lower_changed, int64_t lo, int64_t hi, int lane) {
+    if (DET) {
+        bool T = f0 != 0;
+        if (!T) T = a.symmetric ? __any_sync(0xffffffffu, lower_changed) : lower_in_changed(a, v);
+        bool chg = T && cand != cur && (!a.pickless || cand < cur);
+        uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
+        uint32_t ow = __ldcg(&a.lab_new[v]);
+        __syncwarp();
+        if (nw != ow) {
+            if (lane == 0) __stcg(&a.lab_new[v], nw);
+            mark_dependants(a, v, lo, hi, lane, 32);
+        }
+        if (lane == 0) {
+            ctr_add(a.counters, CNT_EVALS_HI, 1ull);
+            ctr_add(a.counters, CNT_ARCS_HI, (unsigned long long)(hi - lo));
+        }
+    } else {
+        if (cand != cur && (!a.pickless || cand < cur)) {
+            if (lane == 0) {
+                __stcg(&a.lab_old[v], cand);
+                ctr_add(a.counters, CNT_DELTA, 1ull);
+            }
+            for (int64_t e = lo + lane; e < hi; e += 32) a.flag_cur[__ldg(&a.tgt[e])] = 1;
+        }
+        if (lane == 0) {
+            ctr_add(a.counters, CNT_EVALS_HI, 1ull);
+            ctr_add(a.counters, CNT_ARCS_HI, (unsigned long long)(hi - lo));
+        }
+    }
+}
+
+// ================================================================== window staging
+// A warp runs 32 sequential streams (one per lane): 32 rows (low degree) or
+// the 32 chunks of one vertex (high degree).  For each window of S steps the
+// warp stages the next <= S arcs of every stream into a padded shared tile
+// [lane][step] -- the concatenated window is loaded with consecutive lanes on
+// consecutive arcs (coalesced targets / weights, 32 independent label
+// gathers per instruction) -- then every lane replays its own S steps in
+// order.  Self-arcs are staged with weight 0 (weights are > 0).
+constexpr int kWinWarps = 4;
+constexpr int kWinThreads = kWinWarps * 32;
+
+template <class W>
+struct WinS {
+    static constexpr int S = sizeof(W) == 4 ? 32 : 16;
+};
+
+template <class W, bool DET, bool GRID, class Consume>
+__device__ __forceinline__ void window_streams(const SweepArgs &a, uint32_t (*s_lab)[WinS<W>::S + 1],
+                                               W (*s_w)[WinS<W>::S + 1], int lane, int64_t start, int64_t len,
+                                               int32_t sv, bool &lower_changed, Consume &&consume) {
+    constexpr int S = WinS<W>::S;
+    constexpr int G = 8;  // staging iterations in flight per lane
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    const uint64_t pol = policy_evict_first();
+    int64_t maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int64_t x = __shfl_xor_sync(0xffffffffu, maxlen, o);
+        maxlen = x > maxlen ? x : maxlen;
+    }
+    for (int64_t s0 = 0; s0 < maxlen; s0 += S) {
+        const int64_t rem = len - s0;
+        const int seg = rem <= 0 ? 0 : (rem >= S ? S : (int)rem);
+        int excl = 0, total = 0, iters;
+        if (GRID) {
+            // stream j's window is staged by iteration j, lane = step (coalesced)
+            iters = 32;
+        } else {
+            int incl = seg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int x = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += x;
+            }
+            excl = incl - seg;
+            total = __shfl_sync(0xffffffffu, incl, 31);
+            iters = (total + 31) >> 5;
+        }
+        for (int j0 = 0; j0 < iters; j0 += G) {
+            int32_t t[G], ov[G];
+            W w[G];
+            int own[G], stp[G];
+            bool ok[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const int j = j0 + u;
+                int o, sp;
+                bool valid;
+                if (GRID) {
+                    o = j & 31;
+                    sp = lane;
+                    const int sj = __shfl_sync(0xffffffffu, seg, o);
+                    valid = j < 32 && lane < sj;
+                } else {
+                    const int va = j * 32 + lane;
+                    o = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        int ex = __shfl_sync(0xffffffffu, excl, (o + step) & 31);
+                        if (o + step < 32 && ex <= va) o += step;
+                    }
+                    sp = va - __shfl_sync(0xffffffffu, excl, o);
+                    valid = va < total;
+                }
+                const int64_t o_start = __shfl_sync(0xffffffffu, start, o);
+                ov[u] = __shfl_sync(0xffffffffu, sv, o);
+                own[u] = o;
+                stp[u] = sp;
+                ok[u] = valid;
+                if (valid) {
+                    const int64_t e = o_start + s0 + sp;
+                    t[u] = ld_stream(&a.tgt[e], pol);
+                    w[u] = ld_stream(&wts[e], pol);
+                } else {
+                    t[u] = 0;
+                    w[u] = (W)0;
+                }
+            }
+            uint32_t L[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                L[u] = 0;
+                if (ok[u] && t[u] != ov[u]) L[u] = DET ? __ldcg(&a.lab_new[t[u]]) : (uint32_t)__ldcg(&a.lab_old[t[u]]);
+            }
+            if (DET) {  // higher neighbour that changed this sweep: its L0
+#pragma unroll
+                for (int u = 0; u < G; ++u)
+                    if (ok[u] && t[u] > ov[u] && (L[u] >> 31)) L[u] = (uint32_t)__ldg(&a.lab_old[t[u]]);
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                if (ok[u]) {
+                    s_lab[own[u]][stp[u]] = L[u];
+                    s_w[own[u]][stp[u]] = (t[u] == ov[u]) ? (W)0 : w[u];
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll 4
+        for (int x = 0; x < seg; ++x) {
+            const W w = s_w[lane][x];
+            const uint32_t L = s_lab[lane][x];
+            const bool valid = w != (W)0;
+            lower_changed |= valid && (L >> 31) != 0;
+            consume(s0 + x, valid, (int32_t)(L & SLPA_LMASK), w);
+        }
+        __syncwarp();
+    }
+}
+
+// ================================================================== direct streaming
+// Every lane streams its own arc range [start, start + len) in 32-byte aligned
+// batches of 8 arcs: one 256-bit load of targets, one (float) or two (double)
+// 256-bit loads of weights, the batch's 8 label gathers issued together, and
+// the next batch's targets / weights requested before the current batch is
+// consumed.  No shared memory and no warp collectives, so lanes of one warp
+// may stream ranges of different lengths.  Arcs of the batch outside the range
+// are masked (the buffers carry tail padding, slpa_internal.cuh); self arcs
+// are passed to `consume` as invalid so chunk positions stay exact.
+constexpr int kBatch = 8;
+
+__device__ __forceinline__ void ld8(const int32_t *p, int32_t (&r)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld8(const uint32_t *p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld8(const float *p, float (&r)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                 : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld8(const double *p, double (&r)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                 : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(r[4]), "=d"(r[5]), "=d"(r[6]), "=d"(r[7])
+                 : "l"(p + 4), "l"(pol));
+}
+__device__ __forceinline__ void ld8_cg(const float *p, float (&r)[8]) {
+    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld8_cg(const double *p, double (&r)[8]) {
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[4]), "=d"(r[5]), "=d"(r[6]), "=d"(r[7]) : "l"(p + 4));
+}
+
+// Unaligned flavour for short ranges (the chunks of a high-degree row): the
+// batches start at `start`, so only the last one is partial; targets and
+// weights are scalar loads that stay in L1 for the lane's next batch.
+template <class W, bool DET, class Consume>
+__device__ __forceinline__ void lane_stream_u(const SweepArgs &a, int64_t start, int64_t len, int32_t v,
+                                              bool &lower_changed, Consume &&consume) {
+    if (len <= 0) return;
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    int32_t t[kBatch];
+    W w[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        const bool in = j < len;
+        t[j] = in ? __ldg(&a.tgt[start + j]) : v;
+        w[j] = in ? __ldg(&wts[start + j]) : (W)0;
+    }
+    for (int64_t x0 = 0;;) {
+        uint32_t L[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            L[j] = 0;
+            if (t[j] != v) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
+        }
+        if (DET) {
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
+        }
+        const int64_t nx = x0 + kBatch;
+        int32_t tn[kBatch];
+        W wn[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {  // next batch requested before this one is consumed
+            const bool in = nx + j < len;
+            tn[j] = in ? __ldg(&a.tgt[start + nx + j]) : v;
+            wn[j] = in ? __ldg(&wts[start + nx + j]) : (W)0;
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (x0 + j < len) {
+                const bool valid = t[j] != v;
+                if (DET) lower_changed |= valid && (L[j] >> 31) != 0;
+                consume(x0 + j, valid, (int32_t)(L[j] & SLPA_LMASK), w[j]);
+            }
+        }
+        if (nx >= len) break;
+        x0 = nx;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            t[j] = tn[j];
+            w[j] = wn[j];
+        }
+    }
+}
+
+// consume(pos, valid, label, w): pos = arc index relative to `start`.
+template <class W, bool DET, class Consume>
+__device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, int64_t len, int32_t v,
+                                            bool &lower_changed, Consume &&consume) {
+    if (len <= 0) return;
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    const uint64_t pol = policy_evict_first();
+    const int64_t end = start + len;
+    int64_t b = start & ~(int64_t)(kBatch - 1);
+    int32_t t[kBatch];
+    W w[kBatch];
+    ld8(a.tgt + b, t, pol);
+    ld8(wts + b, w, pol);
+    for (;;) {
+        uint32_t L[kBatch];
+        unsigned inr = 0, ok = 0;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const int64_t e = b + j;
+            const bool in = e >= start && e < end;
+            const bool valid = in && t[j] != v;
+            inr |= (unsigned)in << j;
+            ok |= (unsigned)valid << j;
+            L[j] = 0;
+            if (valid) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
+        }
+        if (DET) {  // higher neighbour that changed this sweep: its L0
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (((ok >> j) & 1u) && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
+        }
+        const int64_t nb = b + kBatch;
+        int32_t tn[kBatch];
+        W wn[kBatch];
+        const bool more = nb < end;
+        if (more) {
+            ld8(a.tgt + nb, tn, pol);
+            ld8(wts + nb, wn, pol);
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if ((inr >> j) & 1u) {
+                const bool valid = (ok >> j) & 1u;
+                if (DET) lower_changed |= valid && (L[j] >> 31) != 0;
+                consume(b + j - start, valid, (int32_t)(L[j] & SLPA_LMASK), w[j]);
+            }
+        }
+        if (!more) break;
+        b = nb;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            t[j] = tn[j];
+            w[j] = wn[j];
+        }
+    }
+}
+
+// Stage selection: 1 = direct streaming (default), 0 = window staging.
+int stage_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_STAGE");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
+// ================================================================== lane kernels
+// One lane per vertex.  Lane outputs are written per lane; adjacency walks
+// for changed vertices (dependant marks in deterministic mode, neighbour
+// flags in async mode) are done by the whole warp, one changed lane at a
+// time, so they are coalesced instead of 32 divergent row loops.
+template <bool DET>
+__device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t v, int32_t cur, int32_t cand,
+                                            bool T, int64_t lo, int64_t deg, unsigned long long &n_delta) {
+    const int lane = threadIdx.x & 31;
+    bool walk = false;
+    if (go) {
+        if (DET) {
+            const bool chg = T && cand != cur && (!a.pickless || cand < cur);
+            const uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
+            if (nw != __ldcg(&a.lab_new[v])) {
+                __stcg(&a.lab_new[v], nw);
+                walk = true;
+            }
+        } else if (cand != cur && (!a.pickless || cand < cur)) {
+            __stcg(&a.lab_old[v], cand);
+            n_delta = 1;
+            walk = true;
+        }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, walk);
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t vj = __shfl_sync(0xffffffffu, v, j);
+        const int64_t lj = __shfl_sync(0xffffffffu, lo, j);
+        const int64_t hj = lj + __shfl_sync(0xffffffffu, deg, j);
+        if (DET) mark_dependants(a, vj, lj, hj, lane, 32);
+        else
+            for (int64_t e = lj + lane; e < hj; e += 32) a.flag_cur[__ldg(&a.tgt[e])] = 1;
+    }
+}
+
+// MG over one row.  CHUNKED: the R_H chunks of _chunk_bounds (lpa.py:110-118)
+// are cut by arc position while the row streams; each finished chunk is
+// folded into parts[0] right away -- the same replay sequence as
+// sk = parts[0]; sk.merge(parts[1]); ... (lpa.py:179-186, sketch.py:76-91).
+template <int K, bool CHUNKED, class V>
+struct MgLane {
+    static constexpr bool kHasRescan = true;
+    MgSketchDev<K, V> S, part;
+    int k, p;
+    int64_t base, rem, next;
+    __device__ __forceinline__ void init(int k_, int32_t, int64_t deg, int P) {
+        k = K > 0 ? K : k_;
+        S.reset(k);
+        if (CHUNKED) {
+            part.reset(k);
+            p = 0;
+            base = deg / P;
+            rem = deg % P;
+            next = base + (rem > 0 ? 1 : 0);
+        }
+    }
+    __device__ __forceinline__ void end_chunk() {
+        if (p == 0) {
+            S = part;
+        } else {
+#pragma unroll
+            for (int i = 0; i < KArr<K>::v; ++i) {
+                if (K == 0 && i >= k) break;
+                if (part.val[i] > (V)0) S.acc(part.key[i], part.val[i], k);
+            }
+        }
+        part.reset(k);
+        ++p;
+        next += base + (p < rem ? 1 : 0);
+    }
+    template <class W>
+    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, W w) {
+        if (CHUNKED) {
+            if (pos == next) end_chunk();
+            if (valid) part.acc(c, (V)w, k);
+        } else if (valid) {
+            S.acc(c, (V)w, k);
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (CHUNKED) end_chunk();
+    }
+    __device__ __forceinline__ void rescan_begin() { S.clear_values(k); }
+    template <class W>
+    __device__ __forceinline__ void rescan(int32_t c, W w) { S.rescan_add(c, (V)w, k); }
+    __device__ __forceinline__ int32_t result(int32_t cur) const {
+        int32_t b;
+        return S.max_key(k, b) ? b : cur;  // lpa.py:192-193
+    }
+};
+
+// BM over one row: one BmState(cur, 0) per chunk, reduce_votes pair-max
+// (lpa.py:137-150); unchunked rows are a single vote.
+template <bool CHUNKED, class V>
+struct BmLane {
+    static constexpr bool kHasRescan = false;
+    BmVote<V> st, best;
+    int32_t cur0;
+    int p;
+    int64_t base, rem, next;
+    __device__ __forceinline__ void init(int, int32_t cur, int64_t deg, int P) {
+        cur0 = cur;
+        st = BmVote<V>{cur, (V)0};
+        if (CHUNKED) {
+            p = 0;
+            base = deg / P;
+            rem = deg % P;
+            next = base + (rem > 0 ? 1 : 0);
+        }
+    }
+    __device__ __forceinline__ void end_chunk() {
+        if (p == 0 || bm_better(st.w, st.cand, best.w, best.cand)) best = st;
+        st = BmVote<V>{cur0, (V)0};
+        ++p;
+        next += base + (p < rem ? 1 : 0);
+    }
+    template <class W>
+    __device__ __forceinline__ void on(int64_t pos, bool valid, int32_t c, W w) {
+        if (CHUNKED && pos == next) end_chunk();
+        if (valid) st.acc(c, (V)w);
+    }
+    __device__ __forceinline__ void finish() {
+        if (CHUNKED) end_chunk();
+        else best = st;
+    }
+    __device__ __forceinline__ void rescan_begin() {}
+    template <class W>
+    __device__ __forceinline__ void rescan(int32_t, W) {}
+    __device__ __forceinline__ int32_t result(int32_t) const { return best.cand; }
+};
+
+template <class W, class Pol, bool DET>
+__global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int32_t *__restrict__ list,
+                                                          int64_t count, int round0) {
+    constexpr int S = WinS<W>::S;
+    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
+    __shared__ W s_w[kWinWarps][32][S + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int32_t v = -1;
+    uint8_t f0 = 0;
+    bool go = false;
+    if (i < count) {
+        v = __ldg(&list[i]);
+        f0 = a.flag_cur[v];
+        go = DET ? (!round0 || f0) : (f0 != 0);
+    }
+    int64_t lo = 0, deg = 0;
+    int32_t cur = 0;
+    if (go) {
+        if (!DET) a.flag_cur[v] = 0;
+        lo = __ldg(&a.off[v]);
+        deg = __ldg(&a.off[v + 1]) - lo;
+        cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    }
+    Pol pol;
+    pol.init(a.k, cur, deg, a.parts);
+    bool lower_changed = false;
+    window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, lower_changed,
+                                  [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
+    if (go && deg) pol.finish();
+    if (Pol::kHasRescan && a.scan_double) {
+        pol.rescan_begin();
+        bool dummy = false;
+        window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, dummy,
+                                      [&](int64_t, bool valid, int32_t c, W w) {
+                                          if (valid) pol.rescan(c, w);
+                                      });
+    }
+    unsigned long long n_delta = 0;
+    const int32_t cand = (go && deg) ? pol.result(cur) : cur;
+    const bool T = go && (f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v)));
+    lane_finish<DET>(a, go, v, cur, cand, T, lo, deg, n_delta);
+    warp_count(a.counters, go ? 1ull : 0ull, (unsigned long long)deg, n_delta);
+}
+
+// Same evaluation as k_lane_win, every lane streaming its own row directly.
+template <class W, class Pol, bool DET>
+__global__ void __launch_bounds__(kThreads) k_lane_direct(SweepArgs a, const int32_t *__restrict__ list,
+                                                          int64_t count, int round0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int32_t v = -1;
+    uint8_t f0 = 0;
+    bool go = false;
+    if (i < count) {
+        v = __ldg(&list[i]);
+        f0 = a.flag_cur[v];
+        go = DET ? (!round0 || f0) : (f0 != 0);
+    }
+    int64_t lo = 0, deg = 0;
+    int32_t cur = 0;
+    if (go) {
+        if (!DET) a.flag_cur[v] = 0;
+        lo = __ldg(&a.off[v]);
+        deg = __ldg(&a.off[v + 1]) - lo;
+        cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    }
+    Pol pol;
+    pol.init(a.k, cur, deg, a.parts);
+    bool lower_changed = false;
+    lane_stream<W, DET>(a, lo, deg, v, lower_changed,
+                        [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
+    if (go && deg) pol.finish();
+    if (Pol::kHasRescan && a.scan_double) {
+        pol.rescan_begin();
+        bool dummy = false;
+        lane_stream<W, DET>(a, lo, deg, v, dummy, [&](int64_t, bool valid, int32_t c, W w) {
+            if (valid) pol.rescan(c, w);
+        });
+    }
+    unsigned long long n_delta = 0;
+    const int32_t cand = (go && deg) ? pol.result(cur) : cur;
+    const bool T = go && (f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v)));
+    lane_finish<DET>(a, go, v, cur, cand, T, lo, deg, n_delta);
+    warp_count(a.counters, go ? 1ull : 0ull, (unsigned long long)deg, n_delta);
+}
+
+// Ordered merge of the lanes' part sketches (lane q = parts[b0 + q]) into the
+// slot-parallel warp sketch: sk = parts[0]; sk.merge(parts[1]); ...
+// (lpa.py:179-186, sketch.py:76-91).
+template <int K, class V>
+__device__ __forceinline__ void warp_merge_parts(WarpSketch<V> &S_, const MgSketchDev<K, V> &part, int b0, int P,
+                                                 int k, int lane) {
+    int first = 0;
+    if (b0 == 0) {  // sk = parts[0]
+#pragma unroll
+        for (int i = 0; i < KArr<K>::v; ++i) {
+            if (K == 0 && i >= k) break;
+            int32_t kk = __shfl_sync(0xffffffffu, part.key[i], 0);
+            V vv = __shfl_sync(0xffffffffu, part.val[i], 0);
+            if (lane == i) { S_.key = kk; S_.val = vv; }
+        }
+        first = 1;
+    }
+    const int nb = min(32, P - b0);
+    unsigned nz = 0;
+#pragma unroll
+    for (int i = 0; i < KArr<K>::v; ++i) {
+        if (K == 0 && i >= k) break;
+        if (part.val[i] > (V)0) nz |= 1u << (i & 31);
+    }
+    for (int q = first; q < nb; ++q) {
+        const unsigned mq = __shfl_sync(0xffffffffu, nz, q);
+        if (!mq) continue;
+#pragma unroll
+        for (int i = 0; i < KArr<K>::v; ++i) {
+            if (K == 0 && i >= k) break;
+            if (!(mq & (1u << (i & 31)))) continue;
+            int32_t c = __shfl_sync(0xffffffffu, part.key[i], q);
+            V w = __shfl_sync(0xffffffffu, part.val[i], q);
+            S_.acc(lane, k, c, w);
+        }
+    }
+}
+
+// High degree, MG, direct streaming: warp per vertex, lane g streams chunk g.
+template <class W, int K, bool DET, class V>
+__global__ void __launch_bounds__(kThreads) k_mg_hi_direct(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int round0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;  // warp-uniform
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int k = K > 0 ? K : a.k;
+    const int P = a.parts;
+    bool lower_changed = false;
+    WarpSketch<V> S_{0, (V)0};
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        MgSketchDev<K, V> part;
+        part.reset(k);
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
+        lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lower_changed, [&](int64_t, bool valid, int32_t c, W w) {
+            if (valid) part.acc(c, (V)w, k);
+        });
+        __syncwarp();
+        warp_merge_parts<K, V>(S_, part, b0, P, k, lane);
+    }
+    if (a.scan_double) {  // exact per-key re-count in adjacency order
+        S_.val = (V)0;
+        bool dummy = false;
+        for (int64_t base = lo; base < hi; base += 32) {
+            int64_t x = base + lane;
+            int32_t c = 0;
+            V w = (V)0;
+            bool ok = false;
+            if (x < hi) {
+                int32_t t = __ldg(&a.tgt[x]);
+                if (t != v) {
+                    ok = true;
+                    c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
+                    w = (V)arc_weight<W>(a, x);
+                }
+            }
+            unsigned okm = __ballot_sync(0xffffffffu, ok);
+            while (okm) {
+                int j = __ffs(okm) - 1;
+                okm &= okm - 1;
+                S_.rescan_add(lane, k, __shfl_sync(0xffffffffu, c, j), __shfl_sync(0xffffffffu, w, j));
+            }
+        }
+    }
+    int32_t best;
+    const bool found = S_.max_key(lane, k, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
+}
+
+// High degree, MG, k = 8, R_H <= 32: a warp evaluates kGrp vertices.
+//  (A) per vertex, lane g streams chunk g into a register part sketch and
+//      stores it (physical slots: keys incl. stale ones, values) to shared
+//      memory;
+//  (B) the ordered merge sk = parts[0]; sk.merge(parts[1]); ...
+//      (lpa.py:179-186, sketch.py:76-91) runs for the kGrp vertices at once,
+//      one 8-lane group per vertex, lane = slot: every replayed (key, value)
+//      is one group-wise accumulate (first matching lane, else first empty
+//      lane, else every lane decrements) -- 4 merges for the instructions of
+//      one;
+//  (C) max_key per group, then the warp finishes the vertices one by one.
+constexpr int kGrp = 4;
+constexpr int kGrpWarps = 4;
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const int32_t *__restrict__ list,
+                                                             int64_t count, int round0) {
+    static_assert(sizeof(V) == 4, "grouped merge packs (key, value) in 8 bytes");
+    __shared__ uint2 s_part[kGrpWarps][kGrp][32][8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t first = wid * kGrp;
+    if (first >= count) return;  // warp-uniform
+    const int P = a.parts;
+    uint2(*sp)[32][8] = s_part[wib];
+    int32_t vv[kGrp], cur[kGrp];
+    int64_t lo[kGrp], hi[kGrp];
+    uint8_t f0[kGrp];
+    bool act[kGrp], lch[kGrp];
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+        act[j] = false;
+        lch[j] = false;
+        vv[j] = 0;
+        cur[j] = 0;
+        lo[j] = hi[j] = 0;
+        f0[j] = 0;
+        if (first + j < count) {
+            vv[j] = __ldg(&list[first + j]);
+            f0[j] = a.flag_cur[vv[j]];
+            act[j] = DET ? !(round0 && !f0[j]) : f0[j] != 0;
+        }
+    }
+    __syncwarp();
+    // (A) chunk scans
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+        if (!act[j]) continue;  // warp-uniform
+        const int32_t v = vv[j];
+        if (!DET && lane == 0) a.flag_cur[v] = 0;
+        lo[j] = __ldg(&a.off[v]);
+        hi[j] = __ldg(&a.off[v + 1]);
+        cur[j] = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+        MgSketchDev<8, V> part;
+        part.reset(8);
+        int64_t cs = 0, ce = 0;
+        if (lane < P) chunk_bounds(hi[j] - lo[j], P, lane, cs, ce);
+        bool lc = false;
+        lane_stream_u<W, DET>(a, lo[j] + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
+            if (valid) part.acc(c, (V)w, 8);
+        });
+        lch[j] = __any_sync(0xffffffffu, lc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sp[j][lane][i] = make_uint2((uint32_t)part.key[i], (uint32_t)part.val[i]);
+    }
+    __syncwarp();
+    // (B) grouped ordered merge; group g = lanes 8g..8g+7 = vertex g, lane = slot
+    const int grp = lane >> 3, slot = lane & 7, gb = grp * 8;
+    const bool gact = act[0] && grp == 0 || act[1] && grp == 1 || act[2] && grp == 2 || act[3] && grp == 3;
+    uint2 e0 = sp[grp][0][slot];
+    int32_t key = (int32_t)e0.x;
+    V val = gact ? (V)e0.y : (V)0;
+    for (int q = 1; q < P; ++q) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint2 e = sp[grp][q][i];
+            const bool live = gact && e.y != 0u;
+            if (!__any_sync(0xffffffffu, live)) continue;
+            const int32_t c = (int32_t)e.x;
+            const V w = (V)e.y;
+            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c)) >> gb) & 0xffu;
+            const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
+            const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
+            const V d = (mm | fm) ? (V)0 : w;
+            if (live) {
+                const bool mine = (sel >> slot) & 1u;
+                if (mine) key = c;
+                val = mine ? val + w : val - (val < d ? val : d);
+            }
+        }
+    }
+    // (C) max_key (sketch.py:93-105) per group
+    bool have = val > (V)0;
+    V bw = have ? val : (V)0;
+    int32_t bk = key;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        const V ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+        if (oh && (!have || ow > bw || (ow == bw && ok < bk))) { bw = ow; bk = ok; have = true; }
+    }
+#pragma unroll
+    for (int j = 0; j < kGrp; ++j) {
+        if (!act[j]) continue;
+        const int32_t best = __shfl_sync(0xffffffffu, bk, j * 8);
+        const int found = __shfl_sync(0xffffffffu, (int)have, j * 8);
+        warp_hi_finish<DET>(a, vv[j], cur[j], found ? best : cur[j], f0[j], lch[j], lo[j], hi[j], lane);
+    }
+}
+
+// High degree, BM, direct streaming.
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kThreads) k_bm_hi_direct(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int round0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int P = a.parts;
+    bool lower_changed = false, have = false;
+    int32_t bc = 0;
+    V bw = (V)0;
+    for (int p = lane; p < P; p += 32) {
+        int64_t cs, ce;
+        chunk_bounds(deg, P, p, cs, ce);
+        BmVote<V> st{cur, (V)0};
+        lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lower_changed, [&](int64_t, bool valid, int32_t c, W w) {
+            if (valid) st.acc(c, (V)w);
+        });
+        if (!have || bm_better(st.w, st.cand, bw, bc)) { bc = st.cand; bw = st.w; have = true; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+        int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        V ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
+    }
+    warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
+}
+
+// High degree, MG: warp per vertex, lane g = chunk g of _chunk_bounds(deg,
+// R_H) (lpa.py:178-183) with a register sketch, streamed through the window
+// tile; then parts[1..] are replayed into parts[0] in order (sketch.py:
+// 76-91) on a slot-parallel warp sketch (lane l = slot l).
+template <class W, int K, bool DET, class V>
+__global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int round0) {
+    constexpr int S = WinS<W>::S;
+    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
+    __shared__ W s_w[kWinWarps][32][S + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;  // warp-uniform
+    if (((a.dbg & 4) && wid != 0) || ((a.dbg & 8) && wid == 0)) return;  // timing experiments only
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int k = K > 0 ? K : a.k;
+    const int P = a.parts;
+    bool lower_changed = false;
+    WarpSketch<V> S_{0, (V)0};
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        MgSketchDev<K, V> part;
+        part.reset(k);
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
+        window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
+                               [&](int64_t, bool valid, int32_t c, double w) {
+                                         if (valid && !(a.dbg & 2)) part.acc(c, w, k);
+                                     });
+        warp_merge_parts<K, V>(S_, part, b0, P, k, lane);
+    }
+    if (a.scan_double) {  // exact per-key re-count in adjacency order
+        S_.val = (V)0;
+        bool dummy = false;
+        for (int64_t base = lo; base < hi; base += 32) {
+            int64_t x = base + lane;
+            int32_t c = 0;
+            V w = (V)0;
+            bool ok = false;
+            if (x < hi) {
+                int32_t t = __ldg(&a.tgt[x]);
+                if (t != v) {
+                    ok = true;
+                    c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
+                    w = (V)arc_weight<W>(a, x);
+                }
+            }
+            unsigned okm = __ballot_sync(0xffffffffu, ok);
+            while (okm) {
+                int j = __ffs(okm) - 1;
+                okm &= okm - 1;
+                int32_t cj = __shfl_sync(0xffffffffu, c, j);
+                V wj = __shfl_sync(0xffffffffu, w, j);
+                S_.rescan_add(lane, k, cj, wj);
+            }
+        }
+    }
+    int32_t best;
+    const bool found = S_.max_key(lane, k, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
+}
+
+// High degree, BM: one vote per chunk, pair-max reduce (lpa.py:143-150).
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int round0) {
+    constexpr int S = WinS<W>::S;
+    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
+    __shared__ W s_w[kWinWarps][32][S + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int P = a.parts;
+    bool lower_changed = false;
+    bool have = false;
+    int32_t bc = 0;
+    V bw = (V)0;
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
+        BmVote<V> st{cur, (V)0};
+        window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
+                               [&](int64_t, bool valid, int32_t c, double w) {
+                                         if (valid) st.acc(c, w);
+                                     });
+        if (p < P && (!have || bm_better(st.w, st.cand, bw, bc))) { bc = st.cand; bw = st.w; have = true; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+        int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        V ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
+    }
+    warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
+}
+
+// ================================================================== giant vertices
+// deg >= giant threshold: a single warp per vertex would walk deg/32 arcs per
+// lane with dependent staging latencies on every window -- the tail of every
+// heavy phase (8 ms for the 406k-degree hub at RMAT s24).  Two kernels:
+//  (A) gather: a block per giant materialises its arcs' (label word, weight)
+//      stream -- lower neighbours' L1|changed, higher neighbours' L0, self
+//      arcs weight 0 -- coalesced and fully parallel;
+//  (B) scan: a warp per giant, lane g replays chunk g from that contiguous
+//      buffer with register double-buffered prefetch, so the per-lane chain
+//      runs at ALU speed; then the ordered merge as in k_mg_hi_win.
+constexpr int kGatherThreads = 256;
+
+// grid (segments, giants): block x of giant y gathers arcs
+// [x * kGatherArcs, (x + 1) * kGatherArcs) of its row, 8 per thread with one
+// 256-bit target load and 8 independent label gathers in flight.
+constexpr int kGatherArcs = kGatherThreads * kBatch;
+
+template <class W, bool DET>
+__global__ void __launch_bounds__(kGatherThreads) k_giant_gather(SweepArgs a, const int32_t *__restrict__ slots,
+                                                                 int64_t count, int round0) {
+    const int64_t gi = blockIdx.y;
+    if (gi >= count) return;
+    const int32_t slot = __ldg(&slots[gi]);
+    const int32_t v = __ldg(&a.giant_bin[slot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET ? (round0 && !f0) : !f0) return;
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    W *gw = reinterpret_cast<W *>(a.gw);
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t base = __ldg(&a.giant_off[slot]) - lo;
+    const int64_t s0 = lo + (int64_t)blockIdx.x * kGatherArcs;
+    if (s0 >= hi) return;
+    const uint64_t pol = policy_evict_first();
+    const int64_t e0 = s0 + (int64_t)threadIdx.x * kBatch;
+    int32_t t[kBatch];
+    W w[kBatch];
+    uint32_t L[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        const int64_t e = e0 + j;
+        t[j] = e < hi ? ld_stream(&a.tgt[e], pol) : v;
+        w[j] = e < hi ? ld_stream(&wts[e], pol) : (W)0;
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        L[j] = 0;
+        if (t[j] != v) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        if (DET && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
+        const int64_t e = e0 + j;
+        if (e < hi) {
+            a.glab[base + e] = L[j];
+            gw[base + e] = t[j] == v ? (W)0 : w[j];
+        }
+    }
+}
+
+// Per-lane replay of [x, end) of a giant's gathered stream: 32-byte aligned
+// 8-element batches (256-bit loads), a ring of D batches in flight so the
+// per-lane sketch chain never waits on memory.  Giants are a handful of
+// warps, so the ring's registers cost no occupancy that matters.
+template <class W, class F>
+__device__ __forceinline__ void giant_stream(const SweepArgs &a, int64_t x, int64_t end, bool &lower_changed, F &&f) {
+    if (x >= end) return;
+    constexpr int D = 4;
+    const W *gw = reinterpret_cast<const W *>(a.gw);
+    uint32_t L[D][kBatch];
+    W w[D][kBatch];
+    const int64_t b0 = x & ~(int64_t)(kBatch - 1);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const int64_t b = b0 + d * kBatch;
+        if (b < end) {
+            ld8(a.glab + b, L[d]);
+            ld8_cg(gw + b, w[d]);
+        }
+    }
+    for (int64_t b = b0; b < end; b += D * kBatch) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int64_t bb = b + d * kBatch;
+            if (bb < end) {
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const int64_t e = bb + j;
+                    if (e >= x && e < end && w[d][j] != (W)0) {
+                        lower_changed |= (L[d][j] >> 31) != 0;
+                        f((int32_t)(L[d][j] & SLPA_LMASK), w[d][j]);
+                    }
+                }
+                const int64_t nb = bb + D * kBatch;
+                if (nb < end) {
+                    ld8(a.glab + nb, L[d]);
+                    ld8_cg(gw + nb, w[d]);
+                }
+            }
+        }
+    }
+}
+
+template <class W, int K, bool DET, class V>
+__global__ void __launch_bounds__(kWinThreads) k_mg_giant(SweepArgs a, const int32_t *__restrict__ slots,
+                                                          int64_t count, int round0) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t slot = __ldg(&slots[wid]);
+    const int32_t v = __ldg(&a.giant_bin[slot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int64_t base = __ldg(&a.giant_off[slot]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int k = K > 0 ? K : a.k;
+    const int P = a.parts;
+    bool lower_changed = false;
+    WarpSketch<V> S_{0, (V)0};
+    for (int b0 = 0; b0 < P; b0 += 32) {
+        const int p = b0 + lane;
+        MgSketchDev<K, V> part;
+        part.reset(k);
+        int64_t cs = 0, ce = 0;
+        if (p < P) chunk_bounds(deg, P, p, cs, ce);
+        giant_stream<W>(a, base + cs, base + ce, lower_changed, [&](int32_t c, W w) { part.acc(c, (V)w, k); });
+        warp_merge_parts<K, V>(S_, part, b0, P, k, lane);
+    }
+    if (a.scan_double) {  // exact per-key re-count in adjacency order, from the gathered stream
+        S_.val = (V)0;
+        const W *gw = reinterpret_cast<const W *>(a.gw);
+        for (int64_t b = 0; b < deg; b += 32) {
+            const int64_t x = b + lane;
+            int32_t c = 0;
+            V w = (V)0;
+            if (x < deg) {
+                w = (V)__ldcg(&gw[base + x]);
+                c = (int32_t)(__ldcg(&a.glab[base + x]) & SLPA_LMASK);
+            }
+            unsigned okm = __ballot_sync(0xffffffffu, w != (V)0);
+            while (okm) {
+                int j = __ffs(okm) - 1;
+                okm &= okm - 1;
+                S_.rescan_add(lane, k, __shfl_sync(0xffffffffu, c, j), __shfl_sync(0xffffffffu, w, j));
+            }
+        }
+    }
+    int32_t best;
+    const bool found = S_.max_key(lane, k, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
+}
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kWinThreads) k_bm_giant(SweepArgs a, const int32_t *__restrict__ slots,
+                                                          int64_t count, int round0) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t slot = __ldg(&slots[wid]);
+    const int32_t v = __ldg(&a.giant_bin[slot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET) {
+        if (round0 && !f0) return;
+    } else {
+        if (!f0) return;
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int64_t base = __ldg(&a.giant_off[slot]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int P = a.parts;
+    bool lower_changed = false, have = false;
+    int32_t bc = 0;
+    V bw = (V)0;
+    for (int p = lane; p < P; p += 32) {
+        int64_t cs, ce;
+        chunk_bounds(deg, P, p, cs, ce);
+        BmVote<V> st{cur, (V)0};
+        giant_stream<W>(a, base + cs, base + ce, lower_changed, [&](int32_t c, W w) { st.acc(c, (V)w); });
+        if (!have || bm_better(st.w, st.cand, bw, bc)) { bc = st.cand; bw = st.w; have = true; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+        int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        V ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
+    }
+    warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
+}
+
+// ================================================================== exact
+// select_label_exact (lpa.py:92-107): per-label totals summed in adjacency
+// order (np.bincount order), argmax = smallest label among ties.  One thread
+// per vertex, O(deg^2) -- the correctness path for the quality baseline.
+template <class W, bool DET>
+__global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                    int round0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
+    int32_t v = 0;
+    uint8_t f0 = 0;
+    bool go = false;
+    if (i < count) {
+        v = __ldg(&list[i]);
+        f0 = a.flag_cur[v];
+        go = DET ? (!round0 || f0) : (f0 != 0);
+    }
+    if (go) {
+        if (!DET) a.flag_cur[v] = 0;
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+        bool lower_changed = false, dummy = false;
+        bool found = false;
+        int32_t best = 0;
+        double bw = 0.0;
+        for (int64_t e1 = lo; e1 < hi; ++e1) {
+            int32_t t1 = __ldg(&a.tgt[e1]);
+            if (t1 == v) continue;
+            int32_t c1 = DET ? det_label(a, t1, v, lower_changed) : async_label(a, t1);
+            bool seen = false;
+            for (int64_t e0 = lo; e0 < e1 && !seen; ++e0) {
+                int32_t t0 = __ldg(&a.tgt[e0]);
+                if (t0 == v) continue;
+                int32_t c0 = DET ? det_label(a, t0, v, dummy) : async_label(a, t0);
+                seen = (c0 == c1);
+            }
+            if (seen) continue;
+            double tot = 0.0;
+            for (int64_t e2 = e1; e2 < hi; ++e2) {
+                int32_t t2 = __ldg(&a.tgt[e2]);
+                if (t2 == v) continue;
+                int32_t c2 = DET ? det_label(a, t2, v, dummy) : async_label(a, t2);
+                if (c2 == c1) tot += arc_weight<W>(a, e2);
+            }
+            if (!found || tot > bw || (tot == bw && c1 < best)) { best = c1; bw = tot; found = true; }
+        }
+        const int32_t cand = found ? best : cur;
+        n_eval = 1;
+        n_arcs = (unsigned long long)(hi - lo);
+        if (DET) {
+            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
+            det_commit_output(a, v, cur, cand, T, lo, hi);
+        } else {
+            async_commit_output(a, v, cur, cand, lo, hi, n_delta);
+        }
+    }
+    warp_count(a.counters, n_eval, n_arcs, n_delta);
+}
+
+int hi_grp_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_HI_GRP");
+        return e ? atoi(e) : 0;
+    }();
+    return m;
+}
+
+template <class W, bool DET, class V>
+KernelSet pick_kernels(const slpa_config *cfg) {
+    if (cfg->variant == SLPA_VARIANT_EXACT)
+        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0};
+    const bool direct = stage_mode() != 0;
+    if (cfg->variant == SLPA_VARIANT_BM) {
+        if (direct)
+            return {k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
+                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1};
+        return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
+                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1};
+    }
+    if (cfg->sketch_slots == 8) {
+        if (direct) {
+            if constexpr (sizeof(V) == 4) {
+                if (hi_grp_mode() && cfg->partial_groups <= 32 && cfg->scan_mode != SLPA_SCAN_DOUBLE)
+                    return {k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
+                            k_mg_hi_grp<W, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads,
+                            kGrpWarps * 32, kGrp};
+            }
+            return {k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
+                    k_mg_hi_direct<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads,
+                    kThreads, 1};
+        }
+        return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
+                k_mg_hi_win<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kWinThreads,
+                kWinThreads, 1};
+    }
+    if (direct)
+        return {k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
+                k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads, kThreads,
+                1};
+    return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
+            k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads, kWinThreads,
+            1};
+}
+
+}  // namespace

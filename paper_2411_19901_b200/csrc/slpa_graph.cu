@@ -634,6 +634,7 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
     // giant gather-buffer offsets: exclusive prefix of the giants' degrees
     g.giant_off.alloc(g.n_giant + 1);
     g.giant_arcs = 0;
+    g.giant_max_deg = 0;
     if (g.n_giant > 0) {
         DevBuf<int64_t> dk;
         dk.alloc(g.n_giant + 1);
@@ -643,7 +644,10 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
         const int64_t nn = g.n_giant + 1;
         cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceScan::ExclusiveSum(tmp, bytes, din, dout, nn, s); });
         CUDA_TRY(cudaMemcpyAsync(&g.giant_arcs, g.giant_off.p + g.n_giant, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        int64_t first2[2] = {0, 0};  // bin_giant is degree-descending: slot 0 is the largest
+        CUDA_TRY(cudaMemcpyAsync(first2, g.giant_off.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
+        g.giant_max_deg = first2[1] - first2[0];
         dk.release();
     }
     g.bin_thr = cfg->degree_threshold;

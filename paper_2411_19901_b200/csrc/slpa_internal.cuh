@@ -42,6 +42,11 @@ struct SlpaError {
         if (!(cond)) throw SlpaError{(code), (msg)}; \
     } while (0)
 
+// Every device buffer carries 64 bytes of tail padding: the streaming kernels
+// read arcs in 32-byte aligned batches (256-bit loads) and mask the lanes past
+// the end of a row, so a batch may overhang the last arc of the array.
+constexpr size_t kDevPadBytes = 64;
+
 template <class T>
 struct DevBuf {
     T *p = nullptr;
@@ -50,7 +55,7 @@ struct DevBuf {
         if (c <= count && p) return;
         release();
         if (c == 0) c = 1;
-        CUDA_TRY(cudaMalloc((void **)&p, c * sizeof(T)));
+        CUDA_TRY(cudaMalloc((void **)&p, c * sizeof(T) + kDevPadBytes));
         count = c;
     }
     void release() {
@@ -122,7 +127,7 @@ struct DeviceGraph {
     DevBuf<uint8_t> cls;
     DevBuf<int32_t> bin_lo, bin_mid, bin_hi, bin_giant;
     DevBuf<int64_t> giant_off;  // exclusive prefix of giant degrees (n_giant + 1)
-    int64_t n_lo = 0, n_mid = 0, n_hi = 0, n_giant = 0, giant_arcs = 0;
+    int64_t n_lo = 0, n_mid = 0, n_hi = 0, n_giant = 0, giant_arcs = 0, giant_max_deg = 0;
     const Csr &act() const { return has_order ? perm : base; }
     const int64_t *off() const { return act().off.p; }
     const int32_t *tgt() const { return act().tgt.p; }
@@ -176,6 +181,28 @@ struct slpa_ctx {
     int32_t part = 0;
     int64_t v_begin = 0, v_end = 0;
 };
+
+// ---------------------------------------------------------------- evaluation kernel sets
+typedef void (*EvalKernel)(SweepArgs, const int32_t *, int64_t, int);
+
+// lo: one lane per vertex, one sketch; mid: one lane per vertex, R_H chunks;
+// hi: one warp per vertex, lane = chunk (or thread-per-vertex for `exact`);
+// giant: gather + warp-per-vertex replay.
+struct KernelSet {
+    EvalKernel lo, mid, hi, gather, giant;
+    int lo_threads, hi_threads;
+    int hi_vpw;  // hi kernel: vertices per warp (0 = one thread per vertex)
+};
+
+// slpa_eval_<weights>_<sketch values>_<mode>.cu
+KernelSet slpa_pick_f32_u32_det(const slpa_config *cfg);
+KernelSet slpa_pick_f32_u32_async(const slpa_config *cfg);
+KernelSet slpa_pick_f32_f64_det(const slpa_config *cfg);
+KernelSet slpa_pick_f32_f64_async(const slpa_config *cfg);
+KernelSet slpa_pick_f64_u32_det(const slpa_config *cfg);
+KernelSet slpa_pick_f64_u32_async(const slpa_config *cfg);
+KernelSet slpa_pick_f64_f64_det(const slpa_config *cfg);
+KernelSet slpa_pick_f64_f64_async(const slpa_config *cfg);
 
 // ---------------------------------------------------------------- host-side helpers
 void slpa_validate_config(const slpa_config *cfg);

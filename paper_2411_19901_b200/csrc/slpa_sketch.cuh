@@ -27,6 +27,21 @@ __device__ __forceinline__ V clamp_sub(V v, V w) {  // max(v - w, 0) as sketch.p
     }
 }
 
+// Key representation.  The reference initialises every key to 0
+// (sketch.py:38) and matches "the first slot whose key equals c, even if
+// empty" (sketch.py:59-65).  A key enters a slot only when no slot holds it,
+// so every key other than the initial 0 occupies at most one slot.  Here a
+// never-written slot holds kNoKey (< 0, never a label) instead of 0, which
+// makes every stored key unique: an arc with label c != 0 matches at most one
+// slot and needs no "first of several" resolution.  Label 0 matches the
+// first slot holding 0 or kNoKey -- exactly the slots holding 0 in the
+// reference -- on a (rare) slow path.  Values, stale keys, slot positions and
+// therefore merge replay order, max_key and the double-scan re-count are
+// identical to the reference's.
+constexpr int32_t kNoKey = -1;
+
+__device__ __forceinline__ bool key_matches(int32_t key, int32_t c) { return key == c || (c == 0 && key < 0); }
+
 // MgSketch (sketch.py:17-137).  K > 0: compile-time slots (registers);
 // K == 0: runtime k <= SLPA_KDYN (local memory).
 template <int K, class V = double>
@@ -37,9 +52,9 @@ struct MgSketchDev {
     __device__ __forceinline__ void reset(int k) {  // MgSketch.__init__ sketch.py:34-39
         if constexpr (K > 0) {
 #pragma unroll
-            for (int i = 0; i < K; ++i) { key[i] = 0; val[i] = (V)0; }
+            for (int i = 0; i < K; ++i) { key[i] = kNoKey; val[i] = (V)0; }
         } else {
-            for (int i = 0; i < k; ++i) { key[i] = 0; val[i] = (V)0; }
+            for (int i = 0; i < k; ++i) { key[i] = kNoKey; val[i] = (V)0; }
         }
     }
 
@@ -48,17 +63,41 @@ struct MgSketchDev {
     // every slot loses w, clamped at 0.
     __device__ __forceinline__ void acc(int32_t c, V w, int k) {
         if constexpr (K > 0) {
+            if (c != 0) {
+                // fast path: the key is unique, so "first match" is "the match"
+                bool any = false;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    const bool h = key[i] == c;
+                    if (h) val[i] += w;
+                    any |= h;
+                }
+                if (any) return;
+                unsigned fm = 0;
+#pragma unroll
+                for (int i = 0; i < K; ++i) fm |= val[i] == (V)0 ? (1u << i) : 0u;
+                if (fm) {
+                    const unsigned sel = fm & (0u - fm);
+#pragma unroll
+                    for (int i = 0; i < K; ++i)
+                        if (sel & (1u << i)) { key[i] = c; val[i] = w; }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < K; ++i) val[i] = clamp_sub(val[i], w);
+                }
+                return;
+            }
             unsigned mm = 0, fm = 0;
 #pragma unroll
             for (int i = 0; i < K; ++i) {
-                mm |= (unsigned)(key[i] == c) << i;
-                fm |= (unsigned)(val[i] == (V)0) << i;
+                mm |= key_matches(key[i], c) ? (1u << i) : 0u;
+                fm |= val[i] == (V)0 ? (1u << i) : 0u;
             }
             if (mm) {
                 const unsigned sel = mm & (0u - mm);
 #pragma unroll
                 for (int i = 0; i < K; ++i)
-                    if (sel & (1u << i)) val[i] += w;
+                    if (sel & (1u << i)) { key[i] = c; val[i] += w; }
             } else if (fm) {
                 const unsigned sel = fm & (0u - fm);
 #pragma unroll
@@ -70,7 +109,7 @@ struct MgSketchDev {
             }
         } else {
             for (int i = 0; i < k; ++i)
-                if (key[i] == c) { val[i] += w; return; }
+                if (key_matches(key[i], c)) { key[i] = c; val[i] += w; return; }
             for (int i = 0; i < k; ++i)
                 if (val[i] == (V)0) { key[i] = c; val[i] = w; return; }
             for (int i = 0; i < k; ++i) val[i] = clamp_sub(val[i], w);
@@ -86,18 +125,20 @@ struct MgSketchDev {
         }
     }
 
-    __device__ __forceinline__ void rescan_add(int32_t c, V w, int k) {  // sketch.py:113-126
+    // rescan_add (sketch.py:113-126): first slot whose key equals c gains w.
+    // The slot keeps kNoKey when c == 0 (values only are re-counted).
+    __device__ __forceinline__ void rescan_add(int32_t c, V w, int k) {
         if constexpr (K > 0) {
             unsigned mm = 0;
 #pragma unroll
-            for (int i = 0; i < K; ++i) mm |= (unsigned)(key[i] == c) << i;
+            for (int i = 0; i < K; ++i) mm |= key_matches(key[i], c) ? (1u << i) : 0u;
             const unsigned sel = mm & (0u - mm);
 #pragma unroll
             for (int i = 0; i < K; ++i)
-                if (sel & (1u << i)) val[i] += w;
+                if (sel & (1u << i)) { key[i] = c; val[i] += w; }
         } else {
             for (int i = 0; i < k; ++i)
-                if (key[i] == c) { val[i] += w; return; }
+                if (key_matches(key[i], c)) { key[i] = c; val[i] += w; return; }
         }
     }
 
@@ -157,10 +198,10 @@ struct WarpSketch {
     V val;
     __device__ __forceinline__ void acc(int lane, int k, int32_t c, V w) {
         const bool live = lane < k;
-        const unsigned mm = __ballot_sync(0xffffffffu, live && key == c);
+        const unsigned mm = __ballot_sync(0xffffffffu, live && key_matches(key, c));
         const unsigned fm = __ballot_sync(0xffffffffu, live && val == (V)0);
         if (mm) {
-            if (lane == __ffs(mm) - 1) val += w;
+            if (lane == __ffs(mm) - 1) { key = c; val += w; }
         } else if (fm) {
             if (lane == __ffs(fm) - 1) { key = c; val = w; }
         } else if (live) {
@@ -168,8 +209,8 @@ struct WarpSketch {
         }
     }
     __device__ __forceinline__ void rescan_add(int lane, int k, int32_t c, V w) {
-        unsigned mm = __ballot_sync(0xffffffffu, lane < k && key == c);
-        if (mm && lane == __ffs(mm) - 1) val += w;
+        unsigned mm = __ballot_sync(0xffffffffu, lane < k && key_matches(key, c));
+        if (mm && lane == __ffs(mm) - 1) { key = c; val += w; }
     }
     // max_key over the lanes; result valid on every lane.
     __device__ __forceinline__ bool max_key(int lane, int k, int32_t &out) const {
