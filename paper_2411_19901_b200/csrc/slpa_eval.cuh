@@ -1203,6 +1203,106 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_giant(SweepArgs a, const int
     warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
 }
 
+// Giant MG, k = 8, R_H <= 32: one block per giant, one 8-lane group per
+// chunk (lane = slot), so every arc of a chunk is a group-wise accumulate of a
+// few instructions (first matching lane, else first empty lane, else every
+// lane decrements) instead of a lane's full register-sketch update: the
+// per-chunk sequential chain -- the critical path of a giant -- gets ~5x
+// shorter.  Then warp 0 replays parts 1.. into parts[0] in order.
+constexpr int kGiantWarps = 8;
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kGiantWarps * 32) k_mg_giant_grp(SweepArgs a, const int32_t *__restrict__ slots,
+                                                                  int64_t count, int round0) {
+    __shared__ int32_t s_key[32][8];
+    __shared__ V s_val[32][8];
+    const int64_t gi = blockIdx.x;
+    if (gi >= count) return;
+    const int32_t gslot = __ldg(&slots[gi]);
+    const int32_t v = __ldg(&a.giant_bin[gslot]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET ? (round0 && !f0) : !f0) return;  // block-uniform
+    if (!DET) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.flag_cur[v] = 0;
+    }
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int grp = lane >> 3, sl = lane & 7, gb = grp * 8;
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int64_t base = __ldg(&a.giant_off[gslot]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int P = a.parts;
+    const int p = wib * 4 + grp;
+    int64_t cs = 0, ce = 0;
+    if (p < P) chunk_bounds(deg, P, p, cs, ce);
+    const W *gw = reinterpret_cast<const W *>(a.gw);
+    int64_t len = ce - cs, maxlen = len;
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+        const int64_t x = __shfl_xor_sync(0xffffffffu, maxlen, o);
+        maxlen = x > maxlen ? x : maxlen;
+    }
+    int32_t key = kNoKey;
+    V val = (V)0;
+    bool lc = false;
+    uint32_t Ln = 0;
+    W wn = (W)0;
+    if (sl < len) {
+        Ln = __ldcg(&a.glab[base + cs + sl]);
+        wn = __ldcg(&gw[base + cs + sl]);
+    }
+    for (int64_t x = 0; x < maxlen; x += 8) {
+        const uint32_t Lx = Ln;
+        const W wx = wn;
+        Ln = 0;
+        wn = (W)0;
+        if (x + 8 + sl < len) {  // next batch of the group requested ahead
+            Ln = __ldcg(&a.glab[base + cs + x + 8 + sl]);
+            wn = __ldcg(&gw[base + cs + x + 8 + sl]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t Lj = __shfl_sync(0xffffffffu, Lx, gb + j);
+            const W wj = __shfl_sync(0xffffffffu, wx, gb + j);
+            const bool live = x + j < len && wj != (W)0;  // group-uniform
+            lc |= live && (Lj >> 31) != 0;
+            const int32_t c = (int32_t)(Lj & SLPA_LMASK);
+            const V w = (V)wj;
+            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c)) >> gb) & 0xffu;
+            const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
+            const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
+            const V d = (mm | fm) ? (V)0 : w;
+            if (live) {
+                const bool mine = (sel >> sl) & 1u;
+                if (mine) key = c;
+                val = mine ? val + w : val - (val < d ? val : d);
+            }
+        }
+    }
+    if (p < P) {
+        s_key[p][sl] = key;
+        s_val[p][sl] = val;
+    }
+    const int lc_any = __syncthreads_or(lc ? 1 : 0);
+    if (wib != 0) return;
+    WarpSketch<V> S_{kNoKey, (V)0};
+    if (lane < 8) {
+        S_.key = s_key[0][lane];
+        S_.val = s_val[0][lane];
+    }
+    for (int q = 1; q < P; ++q) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const V w = s_val[q][i];
+            if (w > (V)0) S_.acc(lane, 8, s_key[q][i], w);
+        }
+    }
+    int32_t best;
+    const bool found = S_.max_key(lane, 8, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lc_any != 0, lo, hi, lane);
+}
+
 template <class W, bool DET, class V>
 __global__ void __launch_bounds__(kWinThreads) k_bm_giant(SweepArgs a, const int32_t *__restrict__ slots,
                                                           int64_t count, int round0) {
@@ -1311,41 +1411,59 @@ int hi_grp_mode() {
     return m;
 }
 
+int giant_grp_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_GIANT_GRP");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
+// Kernel choice per configuration.  Defaults: direct streaming; k = 8 with
+// R_H <= 32 and single scan uses the grouped giant kernel.  The alternatives
+// are kept selectable (SLPA_STAGE, SLPA_HI_GRP, SLPA_GIANT_GRP) so every
+// execution path stays covered by the parity matrix (tests/test_gpu_paths.py).
 template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
     if (cfg->variant == SLPA_VARIANT_EXACT)
-        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0};
+        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0, 0};
     const bool direct = stage_mode() != 0;
     if (cfg->variant == SLPA_VARIANT_BM) {
         if (direct)
             return {k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
-                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1};
+                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1, 0};
         return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
-                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1};
+                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1, 0};
     }
-    if (cfg->sketch_slots == 8) {
-        if (direct) {
-            if constexpr (sizeof(V) == 4) {
-                if (hi_grp_mode() && cfg->partial_groups <= 32 && cfg->scan_mode != SLPA_SCAN_DOUBLE)
-                    return {k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
-                            k_mg_hi_grp<W, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads,
-                            kGrpWarps * 32, kGrp};
-            }
-            return {k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
-                    k_mg_hi_direct<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads,
-                    kThreads, 1};
-        }
+    if (cfg->sketch_slots != 8) {
+        if (direct)
+            return {k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
+                    k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads,
+                    kThreads, 1, 0};
+        return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
+                k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads,
+                kWinThreads, 1, 0};
+    }
+    if (!direct)
         return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
                 k_mg_hi_win<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kWinThreads,
-                kWinThreads, 1};
+                kWinThreads, 1, 0};
+    const bool grouped_ok = cfg->partial_groups <= 32 && cfg->scan_mode != SLPA_SCAN_DOUBLE;
+    KernelSet ks{k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
+                 k_mg_hi_direct<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads, kThreads,
+                 1, 0};
+    if constexpr (sizeof(V) == 4) {
+        if (grouped_ok && hi_grp_mode()) {
+            ks.hi = k_mg_hi_grp<W, DET, V>;
+            ks.hi_threads = kGrpWarps * 32;
+            ks.hi_vpw = kGrp;
+        }
     }
-    if (direct)
-        return {k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
-                k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads, kThreads,
-                1};
-    return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
-            k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads, kWinThreads,
-            1};
+    if (grouped_ok && giant_grp_mode()) {
+        ks.giant = k_mg_giant_grp<W, DET, V>;
+        ks.giant_threads = kGiantWarps * 32;
+    }
+    return ks;
 }
 
 }  // namespace

@@ -191,7 +191,8 @@ typedef void (*EvalKernel)(SweepArgs, const int32_t *, int64_t, int);
 struct KernelSet {
     EvalKernel lo, mid, hi, gather, giant;
     int lo_threads, hi_threads;
-    int hi_vpw;  // hi kernel: vertices per warp (0 = one thread per vertex)
+    int hi_vpw;         // hi kernel: vertices per warp (0 = one thread per vertex)
+    int giant_threads;  // giant kernel: block per giant of this size (0 = warp per giant)
 };
 
 // slpa_eval_<weights>_<sketch values>_<mode>.cu

@@ -286,7 +286,10 @@ void launch_giant(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const 
     timed_launch(ctx, SLPA_PROF_EVAL_GIANT, 2, [&] {
         const dim3 grid((unsigned)((ctx->g.giant_max_deg + kGatherArcs - 1) / kGatherArcs), (unsigned)cnt);
         ks.gather<<<grid, kGatherThreads, 0, gs>>>(a, slots, cnt, round0);
-        ks.giant<<<grid_for(cnt * 32, kWinThreads), kWinThreads, 0, gs>>>(a, slots, cnt, round0);
+        if (ks.giant_threads)
+            ks.giant<<<(unsigned)cnt, ks.giant_threads, 0, gs>>>(a, slots, cnt, round0);
+        else
+            ks.giant<<<grid_for(cnt * 32, kWinThreads), kWinThreads, 0, gs>>>(a, slots, cnt, round0);
         CUDA_TRY(cudaGetLastError());
     });
     if (overlap) {
@@ -306,6 +309,15 @@ void launch_filter(cudaStream_t s, const int32_t *bin, int64_t count, const uint
                    unsigned long long *cursor, int as_index = 0) {
     if (count <= 0) return;
     k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor, as_index);
+}
+
+// SLPA_TRACE=1: per-round worklist sizes on stderr (diagnostics only).
+int trace_rounds() {
+    static const int t = [] {
+        const char *e = getenv("SLPA_TRACE");
+        return e ? atoi(e) : 0;
+    }();
+    return t;
 }
 
 __global__ void k_iota(int32_t *out, int64_t n) {
@@ -402,6 +414,9 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             nhi = (int64_t)ctx->h_sum[CNT_HI];
             ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
         }
+        if (trace_rounds())
+            fprintf(stderr, "[slpa] sweep round %lld: lo %lld mid %lld hi %lld giant %lld\n", (long long)rounds,
+                    (long long)nlo, (long long)nmid, (long long)nhi, (long long)ngiant);
         if (nlo == 0 && nmid == 0 && nhi == 0 && ngiant == 0) break;
         pend_any = defer != 0;
         launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);

@@ -51,7 +51,9 @@ ENVS = [
     {"SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
     {"SLPA_HI_SPLIT": "100000"},
     {"SLPA_FORCE_FP64": "1", "SLPA_GIANT": "300"},
-    {"SLPA_HI_GRP": "0", "SLPA_GIANT": "300"},
+    {"SLPA_HI_GRP": "1", "SLPA_GIANT": "300"},
+    {"SLPA_GIANT_GRP": "0", "SLPA_GIANT": "300"},
+    {"SLPA_GIANT": "128"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
 ]
