@@ -97,6 +97,8 @@ void slpa_validate_config(const slpa_config *cfg) {  // LpaConfig.validate (lpa.
     SLPA_REQUIRE(cfg->worker_count >= 0, SLPA_EINVAL, "worker_count must be non-negative");
 }
 
+void set_label_l2_window(slpa_ctx *ctx);
+
 void slpa_alloc_work(slpa_ctx *ctx) {
     const int64_t n = ctx->g.n;
     WorkBuffers &wb = ctx->wb;
@@ -118,6 +120,37 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     if (!ctx->h_counters) CUDA_TRY(cudaMallocHost((void **)&ctx->h_counters, CNT_TOTAL * sizeof(unsigned long long)));
+    set_label_l2_window(ctx);
+}
+
+// Keep the label array the sweeps gather from (lab_new, 4 B per vertex) in
+// L2: an access-policy window on both streams marks it persisting, so the
+// streamed CSR (loaded evict-first) does not push it out.  SLPA_L2_PERSIST_MB
+// caps the set-aside (0 disables).
+void set_label_l2_window(slpa_ctx *ctx) {
+    static const long cap_mb = [] {
+        const char *e = getenv("SLPA_L2_PERSIST_MB");
+        return e ? atol(e) : 60L;
+    }();
+    if (cap_mb <= 0 || ctx->g.n == 0) return;
+    int max_persist = 0, max_window = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+    const size_t want = (size_t)ctx->g.n * sizeof(uint32_t);
+    const size_t setaside = std::min<size_t>((size_t)max_persist, (size_t)cap_mb << 20);
+    if (setaside == 0 || max_window <= 0) return;
+    CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = ctx->wb.lab_new.p;
+    attr.accessPolicyWindow.num_bytes = std::min<size_t>(want, (size_t)max_window);
+    attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)setaside / (float)attr.accessPolicyWindow.num_bytes);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CUDA_TRY(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    if (ctx->stream2) CUDA_TRY(cudaStreamSetAttribute(ctx->stream2, cudaStreamAttributeAccessPolicyWindow, &attr));
+    if (getenv("SLPA_TRACE"))
+        fprintf(stderr, "[slpa] L2 persisting window: %zu bytes of %zu, set-aside %zu (max %d, window max %d)\n",
+                (size_t)attr.accessPolicyWindow.num_bytes, want, setaside, max_persist, max_window);
 }
 
 static void reset_stats(slpa_ctx *ctx) {

@@ -383,6 +383,70 @@ __device__ __forceinline__ void lane_stream_u(const SweepArgs &a, int64_t start,
     }
 }
 
+// Three-stage flavour for long ranges: while batch i is consumed, the label
+// gathers of batch i+1 and the target / weight loads of batch i+2 are in
+// flight, so a long chunk streams at the speed of its sketch chain.
+template <class W, bool DET>
+__device__ __forceinline__ void ld_batch_u(const SweepArgs &a, const W *__restrict__ wts, int64_t start, int64_t x,
+                                           int64_t len, int32_t v, int32_t (&t)[kBatch], W (&w)[kBatch]) {
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        const bool in = x + j < len;
+        t[j] = in ? __ldg(&a.tgt[start + x + j]) : v;
+        w[j] = in ? __ldg(&wts[start + x + j]) : (W)0;
+    }
+}
+
+template <bool DET>
+__device__ __forceinline__ void gather_batch(const SweepArgs &a, int32_t v, const int32_t (&t)[kBatch],
+                                             uint32_t (&L)[kBatch]) {
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        L[j] = 0;
+        if (t[j] != v) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
+    }
+}
+
+template <class W, bool DET, class Consume>
+__device__ __forceinline__ void lane_stream_p(const SweepArgs &a, int64_t start, int64_t len, int32_t v,
+                                              bool &lower_changed, Consume &&consume) {
+    if (len <= 0) return;
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    int32_t tA[kBatch], tB[kBatch], tC[kBatch];
+    W wA[kBatch], wB[kBatch], wC[kBatch];
+    uint32_t LA[kBatch], LB[kBatch];
+    ld_batch_u<W, DET>(a, wts, start, 0, len, v, tA, wA);
+    gather_batch<DET>(a, v, tA, LA);
+    ld_batch_u<W, DET>(a, wts, start, kBatch, len, v, tB, wB);
+    for (int64_t x0 = 0;;) {
+        gather_batch<DET>(a, v, tB, LB);                                // batch i+1 (masked past the end)
+        ld_batch_u<W, DET>(a, wts, start, x0 + 2 * kBatch, len, v, tC, wC);  // batch i+2
+        if (DET) {
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (tA[j] > v && (LA[j] >> 31)) LA[j] = (uint32_t)__ldg(&a.lab_old[tA[j]]);
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (x0 + j < len) {
+                const bool valid = tA[j] != v;
+                if (DET) lower_changed |= valid && (LA[j] >> 31) != 0;
+                consume(x0 + j, valid, (int32_t)(LA[j] & SLPA_LMASK), wA[j]);
+            }
+        }
+        x0 += kBatch;
+        if (x0 >= len) break;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            tA[j] = tB[j];
+            wA[j] = wB[j];
+            LA[j] = LB[j];
+            tB[j] = tC[j];
+            wB[j] = wC[j];
+        }
+    }
+}
+
 // consume(pos, valid, label, w): pos = arc index relative to `start`.
 template <class W, bool DET, class Consume>
 __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, int64_t len, int32_t v,
@@ -879,6 +943,114 @@ __global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const
         const int found = __shfl_sync(0xffffffffu, (int)have, j * 8);
         warp_hi_finish<DET>(a, vv[j], cur[j], found ? best : cur[j], f0[j], lch[j], lo[j], hi[j], lane);
     }
+}
+
+// High degree, MG, k = 8, R_H <= 32, integer sketch values: lane-parallel
+// merge in two launches.
+//  k_mg_hi_scan: a warp per vertex (lane g = chunk g, register sketch) stores
+//    its 32 part sketches (keys then values, physical slots) to scratch
+//    indexed by worklist position, plus (cur, f0, lower_changed);
+//  k_mg_hi_merge: LANE j = worklist entry j replays parts[1..] into parts[0]
+//    in order through a register sketch (lpa.py:179-186, sketch.py:76-91) --
+//    32 merges for the instructions of one warp-wide merge -- then the warp
+//    finishes its 32 vertices (label word, dependant marks) cooperatively.
+constexpr int kLpmWords = 32 * 16;  // 32 parts x (8 keys + 8 values)
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kThreads) k_mg_hi_scan(SweepArgs a, const int32_t *__restrict__ list,
+                                                         int64_t count, int round0) {
+    static_assert(sizeof(V) == 4, "scratch holds 32-bit values");
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;  // warp-uniform
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    const bool act = DET ? !(round0 && !f0) : f0 != 0;
+    if (!act) {
+        if (lane == 0) a.hmeta[wid] = make_uint2(0u, 0u);
+        return;
+    }
+    if (!DET) {
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    MgSketchDev<8, V> part;
+    part.reset(8);
+    int64_t cs = 0, ce = 0;
+    if (lane < a.parts) chunk_bounds(hi - lo, a.parts, lane, cs, ce);
+    bool lc = false;
+    if (a.stream == 1)
+        lane_stream_p<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
+            if (valid) part.acc(c, (V)w, 8);
+        });
+    else
+        lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
+            if (valid) part.acc(c, (V)w, 8);
+        });
+    const bool lca = __any_sync(0xffffffffu, lc);
+    uint32_t *dst = a.hparts + (size_t)wid * kLpmWords;
+    uint4 *kd = reinterpret_cast<uint4 *>(dst + lane * 8);
+    uint4 *vd = reinterpret_cast<uint4 *>(dst + 256 + lane * 8);
+    kd[0] = make_uint4((uint32_t)part.key[0], (uint32_t)part.key[1], (uint32_t)part.key[2], (uint32_t)part.key[3]);
+    kd[1] = make_uint4((uint32_t)part.key[4], (uint32_t)part.key[5], (uint32_t)part.key[6], (uint32_t)part.key[7]);
+    vd[0] = make_uint4((uint32_t)part.val[0], (uint32_t)part.val[1], (uint32_t)part.val[2], (uint32_t)part.val[3]);
+    vd[1] = make_uint4((uint32_t)part.val[4], (uint32_t)part.val[5], (uint32_t)part.val[6], (uint32_t)part.val[7]);
+    if (lane == 0) a.hmeta[wid] = make_uint2((uint32_t)cur, 1u | (f0 ? 2u : 0u) | (lca ? 4u : 0u));
+}
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kThreads) k_mg_hi_merge(SweepArgs a, const int32_t *__restrict__ list,
+                                                          int64_t count, int) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= count) return;
+    const uint2 meta = __ldcg(&a.hmeta[idx]);
+    if (!(meta.y & 1u)) return;
+    const uint32_t *src = a.hparts + (size_t)idx * kLpmWords;
+    MgSketchDev<8, V> S;
+    uint32_t kk[8], vv[8], kn[8], vn[8];
+    ld8(src, kk);
+    ld8(src + 256, vv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        S.key[i] = (int32_t)kk[i];
+        S.val[i] = (V)vv[i];
+    }
+    ld8(src + 8, kk);
+    ld8(src + 256 + 8, vv);
+    for (int q = 1; q < a.parts; ++q) {
+        if (q + 1 < a.parts) {  // next part requested before this one is replayed
+            ld8(src + (q + 1) * 8, kn);
+            ld8(src + 256 + (q + 1) * 8, vn);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (vv[i] != 0u) S.acc((int32_t)kk[i], (V)vv[i], 8);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            kk[i] = kn[i];
+            vv[i] = vn[i];
+        }
+    }
+    int32_t best;
+    const int32_t cand = S.max_key(8, best) ? best : (int32_t)meta.x;
+    a.hparts[(size_t)idx * kLpmWords] = (uint32_t)cand;  // part 0's first key is no longer needed
+}
+
+// Finish of the merged vertices: a warp per entry, as k_mg_hi_direct.
+template <bool DET>
+__global__ void __launch_bounds__(kThreads) k_mg_hi_finish(SweepArgs a, const int32_t *__restrict__ list,
+                                                           int64_t count, int) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;
+    const uint2 meta = __ldcg(&a.hmeta[wid]);
+    if (!(meta.y & 1u)) return;
+    const int32_t v = __ldg(&list[wid]);
+    const int32_t cand = (int32_t)__ldcg(&a.hparts[(size_t)wid * kLpmWords]);
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    warp_hi_finish<DET>(a, v, (int32_t)meta.x, cand, (meta.y & 2u) ? 1 : 0, (meta.y & 4u) != 0, lo, hi, lane);
 }
 
 // High degree, BM, direct streaming.
@@ -1406,7 +1578,7 @@ __global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *
 int hi_grp_mode() {
     static const int m = [] {
         const char *e = getenv("SLPA_HI_GRP");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 2;
     }();
     return m;
 }
@@ -1426,37 +1598,43 @@ int giant_grp_mode() {
 template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
     if (cfg->variant == SLPA_VARIANT_EXACT)
-        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0, 0};
+        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0, 0, nullptr, nullptr};
     const bool direct = stage_mode() != 0;
     if (cfg->variant == SLPA_VARIANT_BM) {
         if (direct)
             return {k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
-                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1, 0};
+                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1, 0, nullptr, nullptr};
         return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
-                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1, 0};
+                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1, 0, nullptr, nullptr};
     }
     if (cfg->sketch_slots != 8) {
         if (direct)
             return {k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
                     k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads,
-                    kThreads, 1, 0};
+                    kThreads, 1, 0, nullptr, nullptr};
         return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
                 k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads,
-                kWinThreads, 1, 0};
+                kWinThreads, 1, 0, nullptr, nullptr};
     }
     if (!direct)
         return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
                 k_mg_hi_win<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kWinThreads,
-                kWinThreads, 1, 0};
+                kWinThreads, 1, 0, nullptr, nullptr};
     const bool grouped_ok = cfg->partial_groups <= 32 && cfg->scan_mode != SLPA_SCAN_DOUBLE;
     KernelSet ks{k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
                  k_mg_hi_direct<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads, kThreads,
-                 1, 0};
+                 1, 0, nullptr, nullptr};
     if constexpr (sizeof(V) == 4) {
-        if (grouped_ok && hi_grp_mode()) {
+        if (grouped_ok && hi_grp_mode() == 1) {
             ks.hi = k_mg_hi_grp<W, DET, V>;
             ks.hi_threads = kGrpWarps * 32;
             ks.hi_vpw = kGrp;
+        } else if (grouped_ok && hi_grp_mode() == 2) {
+            if (DET) {  // async keeps the fused kernel: labels move within the launch
+                ks.hi = k_mg_hi_scan<W, DET, V>;
+                ks.hi_merge = k_mg_hi_merge<W, DET, V>;
+                ks.hi_finish = k_mg_hi_finish<DET>;
+            }
         }
     }
     if (grouped_ok && giant_grp_mode()) {

@@ -539,7 +539,7 @@ void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order, bool on_device)
 static int64_t giant_split() {
     static int64_t v = [] {
         const char *e = getenv("SLPA_GIANT");
-        return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)65536;
+        return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)32768;
     }();
     return v;
 }

@@ -88,10 +88,13 @@ struct SweepArgs {
     int32_t thr;                      // degree_threshold (chunked evaluation at deg >= thr)
     int32_t single;                   // shared_sketch: one sketch over any degree
     int32_t dbg;                      // timing experiments only (SLPA_DEBUG_SKIP); 0 in production
+    int32_t stream;                   // high-degree chunk streaming: 1 = three-stage pipeline, 0 = two-stage
     const int32_t *giant_bin;         // giant vertices (deg >= giant threshold), degree desc
     const int64_t *giant_off;         // exclusive prefix of their degrees
     uint32_t *glab;                   // gathered label words of their arcs
     void *gw;                         // gathered weights (W)
+    uint32_t *hparts;                 // high degree, lane-parallel merge: part sketches per worklist entry
+    uint2 *hmeta;                     //   (cur label, active | f0 << 1 | lower_changed << 2) per entry
 };
 
 enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_GIANT = 8, CNT_N = 9 };
@@ -145,6 +148,8 @@ struct WorkBuffers {
     DevBuf<uint8_t> flag_a, flag_b;
     DevBuf<uint32_t> dirty_a, dirty_b;
     DevBuf<int32_t> wl_lo, wl_mid, wl_hi, wl_giant;
+    DevBuf<uint32_t> hparts;      // lane-parallel merge scratch (high degree)
+    DevBuf<uint2> hmeta;
     DevBuf<uint32_t> glab;        // giant gather buffers
     DevBuf<unsigned char> gw;
     DevBuf<int32_t> io_labels;  // staging for host <-> device label exchange
@@ -155,7 +160,7 @@ struct WorkBuffers {
     DevBuf<unsigned char> scratch;  // cub temp storage
     size_t bytes() const {
         return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() +
-               dirty_b.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
+               dirty_b.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
     }
 };
@@ -193,6 +198,8 @@ struct KernelSet {
     int lo_threads, hi_threads;
     int hi_vpw;         // hi kernel: vertices per warp (0 = one thread per vertex)
     int giant_threads;  // giant kernel: block per giant of this size (0 = warp per giant)
+    EvalKernel hi_merge;   // non-null: `hi` is a scan writing part sketches, this kernel merges them
+    EvalKernel hi_finish;  //   and this one (a warp per vertex) commits the merged candidates
 };
 
 // slpa_eval_<weights>_<sketch values>_<mode>.cu

@@ -24,6 +24,15 @@
 
 namespace {
 
+// SLPA_TRACE=1: per-round worklist sizes on stderr (diagnostics only).
+int trace_rounds() {
+    static const int t = [] {
+        const char *e = getenv("SLPA_TRACE");
+        return e ? atoi(e) : 0;
+    }();
+    return t;
+}
+
 // ================================================================== round plumbing
 // Round 0 with heavy vertices deferred from the start: flagged heavy
 // vertices go straight to the pending bitmap.
@@ -96,9 +105,13 @@ __global__ void __launch_bounds__(kThreads) k_commit_lo(SweepArgs a, const int32
             a.lab_new[v] = (uint32_t)c;
             d = 1;
             const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-            for (int64_t e = lo; e < hi; ++e) {
-                int32_t t = __ldg(&a.tgt[e]);
-                if (t <= v) a.flag_next[t] = 1;
+            for (int64_t e0 = lo; e0 < hi; e0 += 8) {  // 8 independent target loads in flight
+                int32_t t[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) t[j] = e0 + j < hi ? __ldg(&a.tgt[e0 + j]) : INT32_MAX;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (t[j] <= v) a.flag_next[t[j]] = 1;
             }
         }
     }
@@ -209,6 +222,11 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         return e ? atoi(e) : 0;
     }();
     a.dbg = dbg;
+    static const int stream = [] {
+        const char *e = getenv("SLPA_STREAM");
+        return e ? atoi(e) : 1;
+    }();
+    a.stream = stream;
     a.giant_bin = g.bin_giant.p;
     a.giant_off = g.giant_off.p;
     a.glab = ctx->wb.glab.p;
@@ -250,6 +268,10 @@ void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn) {
     ctx->prof.ms[cls] += ms;
     ctx->prof.evals[cls] += (int64_t)(ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI] - e0);
     ctx->prof.arcs[cls] += (int64_t)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI] - a0);
+    if (trace_rounds() >= 2)
+        fprintf(stderr, "[slpa]   launch class %d: %.3f ms, %lld evals, %lld arcs\n", cls, ms,
+                (long long)(ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI] - e0),
+                (long long)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI] - a0));
 }
 
 void launch_lane(slpa_ctx *ctx, EvalKernel k, int threads, const SweepArgs &a, const int32_t *list, int64_t cnt,
@@ -264,9 +286,22 @@ void launch_lane(slpa_ctx *ctx, EvalKernel k, int threads, const SweepArgs &a, c
 void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
                int cls) {
     if (cnt <= 0) return;
-    timed_launch(ctx, cls, 1, [&] {
+    SweepArgs aa = a;
+    if (ks.hi_merge) {  // scratch for the lane-parallel merge (sized for the whole high-degree bin)
+        WorkBuffers &wb = ctx->wb;
+        const int64_t cap = ctx->g.n_hi;
+        wb.hparts.alloc((size_t)cap * kLpmWords);
+        wb.hmeta.alloc((size_t)cap);
+        aa.hparts = wb.hparts.p;
+        aa.hmeta = wb.hmeta.p;
+    }
+    timed_launch(ctx, cls, ks.hi_merge ? 3 : 1, [&] {
         const int64_t items = ks.hi_vpw ? (cnt + ks.hi_vpw - 1) / ks.hi_vpw * 32 : cnt;
-        ks.hi<<<grid_for(items, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(a, list, cnt, round0);
+        ks.hi<<<grid_for(items, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(aa, list, cnt, round0);
+        if (ks.hi_merge) {
+            ks.hi_merge<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(aa, list, cnt, round0);
+            ks.hi_finish<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(aa, list, cnt, round0);
+        }
         CUDA_TRY(cudaGetLastError());
     });
 }
@@ -309,15 +344,6 @@ void launch_filter(cudaStream_t s, const int32_t *bin, int64_t count, const uint
                    unsigned long long *cursor, int as_index = 0) {
     if (count <= 0) return;
     k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor, as_index);
-}
-
-// SLPA_TRACE=1: per-round worklist sizes on stderr (diagnostics only).
-int trace_rounds() {
-    static const int t = [] {
-        const char *e = getenv("SLPA_TRACE");
-        return e ? atoi(e) : 0;
-    }();
-    return t;
 }
 
 __global__ void k_iota(int32_t *out, int64_t n) {

@@ -52,8 +52,11 @@ ENVS = [
     {"SLPA_HI_SPLIT": "100000"},
     {"SLPA_FORCE_FP64": "1", "SLPA_GIANT": "300"},
     {"SLPA_HI_GRP": "1", "SLPA_GIANT": "300"},
+    {"SLPA_HI_GRP": "0", "SLPA_GIANT": "300"},
     {"SLPA_GIANT_GRP": "0", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "128"},
+    {"SLPA_STREAM": "0", "SLPA_GIANT": "5000"},
+    {"SLPA_L2_PERSIST_MB": "40"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
 ]
