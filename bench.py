@@ -21,8 +21,10 @@ convergence) from fresh labels.
 * cpu_baseline: the CPU oracle (C restatement of the reference) on this
            host, 1 thread, a bounded prefix of sweep 0 on the same graph.
 * N > 1  : one RMAT graph of scale --scale + log2(N) partitioned by contiguous
-           vertex ranges (asynchronous partitioned sweep, NCCL label
-           all-gather + flag max-reduce per sweep); scaling "weak".
+           vertex ranges; deterministic mode (default): speculative rounds
+           across ranks, NCCL all-gather of the owned label words + MAX-reduce
+           of the dirty marks per round (bit-identical to 1 GPU); --mode
+           async: the asynchronous partitioned sweep.  Scaling "weak".
 """
 
 from __future__ import annotations
@@ -201,7 +203,7 @@ def run_partitioned(args, world, rank, local, dist):
     ranges = partition_ranges(n, world)
     eng = slpa.Engine(local)
     eng.part_gen_rmat(scale, *ranges[rank], seed=SEED, permute=True)
-    cfg = slpa.LpaConfig(variant=args.variant, worker_count=1)
+    cfg = slpa.LpaConfig(variant=args.variant, worker_count=0 if args.mode == "det" else 1)
     dev = torch.device(f"cuda:{local}")
     m_local = torch.tensor([eng.m], dtype=torch.int64, device=dev)
     dist.all_reduce(m_local)
@@ -237,7 +239,9 @@ def run_partitioned(args, world, rank, local, dist):
             "config": {"workload": f"nuMG8-LPA RMAT s{scale} ef16 partitioned over {world} GPUs",
                        "graph": f"RMAT scale {scale} (= {args.scale} + log2 N), edge factor 16, permuted, seed {SEED}",
                        "vertices": n, "arcs": m, "variant": args.variant,
-                       "mode": "async (partitioned; deterministic multi-GPU is not implemented)",
+                       "mode": ("deterministic (bit-exact sequential; speculative rounds with a per-round "
+                                "label all-gather + dirty-mark max-reduce)") if args.mode == "det"
+                               else "async (partitioned)",
                        "parallelism": f"{world} contiguous vertex ranges, NCCL label all-gather + flag max-reduce",
                        "l2_policy": "inputs larger than L2"},
             "iterations_per_step": iters_all, "gpu_launches": None, "e2e": None, "roofline": None,

@@ -182,6 +182,19 @@ int32_t slpa_part_begin(slpa_ctx *ctx, const slpa_config *cfg);
 int32_t slpa_part_sweep(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickless, int64_t *changed_local);
 /* After the exchange: clear the remote (outgoing-mark) flag entries. */
 int32_t slpa_part_end_exchange(slpa_ctx *ctx);
+/* Deterministic (worker_count == 0) partitioned sweep, one round per call
+ * (SURVEY §8(e3)): evaluate the owned flagged (round 0) or dirty vertices and
+ * export the dirty marks as bytes; the host then all-gathers the owned ranges
+ * of lab_new and MAX-reduces the dirty bytes (views from
+ * slpa_part_det_buffers), and slpa_part_det_import folds the global marks
+ * back (dirty_total = set marks, identical on every rank; 0 ends the sweep).
+ * slpa_part_det_commit closes the sweep (owned changed-vertex count; the
+ * flags are then MAX-reduced and slpa_part_end_exchange called as in the
+ * asynchronous protocol).  Output is bit-identical to slpa_run. */
+int32_t slpa_part_det_buffers(slpa_ctx *ctx, uint64_t *lab_new_dptr, uint64_t *dirty_bytes_dptr);
+int32_t slpa_part_det_round(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickless, int32_t round);
+int32_t slpa_part_det_import(slpa_ctx *ctx, int64_t *dirty_total);
+int32_t slpa_part_det_commit(slpa_ctx *ctx, const slpa_config *cfg, int64_t *changed_local);
 /* Rank-local tallies: internal weight (scalar) and device float64[n]
  * incident / int64[n] sizes arrays for an all-reduce; then Q from the
  * reduced incident array and the summed internal weight. */

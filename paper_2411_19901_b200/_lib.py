@@ -102,6 +102,10 @@ SIGNATURES = {
     "slpa_part_begin": (_i32, [_vp, ctypes.POINTER(SlpaConfig)]),
     "slpa_part_sweep": (_i32, [_vp, ctypes.POINTER(SlpaConfig), _i32, ctypes.POINTER(_i64)]),
     "slpa_part_end_exchange": (_i32, [_vp]),
+    "slpa_part_det_buffers": (_i32, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "slpa_part_det_round": (_i32, [_vp, ctypes.POINTER(SlpaConfig), _i32, _i32]),
+    "slpa_part_det_import": (_i32, [_vp, ctypes.POINTER(_i64)]),
+    "slpa_part_det_commit": (_i32, [_vp, ctypes.POINTER(SlpaConfig), ctypes.POINTER(_i64)]),
     "slpa_part_tally": (_i32, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "slpa_part_modularity": (_i32, [_vp, _d, ctypes.POINTER(_d)]),
 }

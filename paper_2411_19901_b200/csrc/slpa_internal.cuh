@@ -147,6 +147,8 @@ struct WorkBuffers {
     DevBuf<uint32_t> lab_new;
     DevBuf<uint8_t> flag_a, flag_b;
     DevBuf<uint32_t> dirty_a, dirty_b;
+    DevBuf<uint8_t> dirty_bytes;  // multi-GPU deterministic: dirty marks exchanged as bytes
+    DevBuf<unsigned long long> dcount;
     DevBuf<int32_t> wl_lo, wl_mid, wl_hi, wl_giant;
     DevBuf<uint32_t> hparts;      // lane-parallel merge scratch (high degree)
     DevBuf<uint2> hmeta;
@@ -159,7 +161,7 @@ struct WorkBuffers {
     DevBuf<unsigned long long> metric_u;
     DevBuf<unsigned char> scratch;  // cub temp storage
     size_t bytes() const {
-        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() +
+        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() +
                dirty_b.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
     }
@@ -223,6 +225,9 @@ void slpa_assemble_unit_edges(slpa_ctx *ctx, int64_t n, int64_t num_edges, uint3
 // sweep drivers (slpa_sweep.cu)
 int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless);
 int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless);
+void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickless, int round);
+int64_t slpa_part_det_import_impl(slpa_ctx *ctx);
+int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg);
 void slpa_init_labels(slpa_ctx *ctx);  // lab = ids (or arange), flags = 1
 void slpa_labels_to_host(slpa_ctx *ctx, int32_t *host);       // by original id
 void slpa_labels_from_host(slpa_ctx *ctx, const int32_t *host);

@@ -138,15 +138,16 @@ int32_t slpa_part_buffers(slpa_ctx *ctx, uint64_t *labels_dptr, uint64_t *flags_
 }
 
 // Start a partitioned lpa_run: labels = arange(n) (lpa.py:289), owned
-// vertices unprocessed (lpa.py:290), no outgoing marks.
+// vertices unprocessed (lpa.py:290), no outgoing marks.  worker_count > 0:
+// asynchronous sweeps (slpa_part_sweep); worker_count == 0: deterministic
+// sweeps driven round by round (slpa_part_det_round / _import / _commit).
 int32_t slpa_part_begin(slpa_ctx *ctx, const slpa_config *cfg) {
     return guard(ctx, [&] {
         slpa_validate_config(cfg);
         require_part(ctx);
-        SLPA_REQUIRE(cfg->worker_count > 0, SLPA_EUNSUPPORTED,
-                     "partitioned (multi-GPU) runs use the asynchronous sweep: set worker_count > 0");
         slpa_ensure_bins(ctx, cfg);
         slpa_alloc_work(ctx);
+        if (cfg->worker_count == 0) ctx->wb.dirty_bytes.alloc((size_t)ctx->g.n);
         ctx->stats = slpa_run_stats{};
         slpa_init_labels(ctx);
         const int64_t n = ctx->g.n;
@@ -165,6 +166,44 @@ int32_t slpa_part_sweep(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickless,
         slpa_ensure_bins(ctx, cfg);
         *changed_local = slpa_sweep_async(ctx, cfg, pickless ? 1 : 0);
         ctx->stats.sweeps += 1;
+    });
+}
+
+int32_t slpa_part_det_buffers(slpa_ctx *ctx, uint64_t *lab_new_dptr, uint64_t *dirty_bytes_dptr) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        SLPA_REQUIRE(ctx->wb.lab_new.p && ctx->wb.dirty_bytes.p, SLPA_EINVAL,
+                     "call slpa_part_begin with worker_count == 0 first");
+        *lab_new_dptr = (uint64_t)(uintptr_t)ctx->wb.lab_new.p;
+        *dirty_bytes_dptr = (uint64_t)(uintptr_t)ctx->wb.dirty_bytes.p;
+    });
+}
+
+int32_t slpa_part_det_round(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickless, int32_t round) {
+    return guard(ctx, [&] {
+        slpa_validate_config(cfg);
+        require_part(ctx);
+        SLPA_REQUIRE(cfg->worker_count == 0, SLPA_EINVAL, "deterministic rounds need worker_count == 0");
+        SLPA_REQUIRE(ctx->wb.dirty_bytes.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
+        slpa_ensure_bins(ctx, cfg);
+        slpa_part_det_round_impl(ctx, cfg, pickless ? 1 : 0, round);
+    });
+}
+
+int32_t slpa_part_det_import(slpa_ctx *ctx, int64_t *dirty_total) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        SLPA_REQUIRE(ctx->wb.dirty_bytes.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
+        *dirty_total = slpa_part_det_import_impl(ctx);
+    });
+}
+
+int32_t slpa_part_det_commit(slpa_ctx *ctx, const slpa_config *cfg, int64_t *changed_local) {
+    return guard(ctx, [&] {
+        slpa_validate_config(cfg);
+        require_part(ctx);
+        SLPA_REQUIRE(ctx->wb.dirty_bytes.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
+        *changed_local = slpa_part_det_commit_impl(ctx, cfg);
     });
 }
 

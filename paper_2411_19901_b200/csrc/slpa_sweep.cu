@@ -346,12 +346,139 @@ void launch_filter(cudaStream_t s, const int32_t *bin, int64_t count, const uint
     k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor, as_index);
 }
 
+// Multi-GPU deterministic sweep: dirty marks cross ranks as bytes (NCCL has
+// no bitwise-OR reduction; a MAX over 0/1 bytes is the OR).
+__global__ void k_dirty_bits_to_bytes(const uint32_t *__restrict__ bits, uint8_t *__restrict__ bytes, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) bytes[i] = (uint8_t)((__ldg(&bits[i >> 5]) >> (i & 31)) & 1u);
+}
+__global__ void k_dirty_bytes_to_bits(const uint8_t *__restrict__ bytes, uint32_t *__restrict__ bits, int64_t n,
+                                      unsigned long long *__restrict__ count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool b = i < n && bytes[i] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0 && i < n) {
+        bits[i >> 5] = m;
+        if (m) atomicAdd(count, (unsigned long long)__popc(m));
+    }
+}
+// Fold L1 into L0 for every vertex of the replica (owned entries were
+// already folded by the commit kernels; this makes the remote ones agree).
+__global__ void k_fold_all(int32_t *lab_old, uint32_t *lab_new, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t w = lab_new[i];
+    if (w & SLPA_CHG) {
+        lab_old[i] = (int32_t)(w & SLPA_LMASK);
+        lab_new[i] = w & SLPA_LMASK;
+    }
+}
+
 __global__ void k_iota(int32_t *out, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = (int32_t)i;
 }
 
 }  // namespace
+
+// ------------------------------------------------------------ multi-GPU deterministic rounds
+// The host (distributed.py) drives a partitioned deterministic sweep round by
+// round: slpa_part_det_round evaluates this rank's owned vertices (round 0:
+// every flagged one; later rounds: the dirty ones) and exports its dirty
+// bitmap as bytes; the host all-gathers the owned lab_new ranges and
+// MAX-reduces the dirty bytes; slpa_part_det_import turns the global marks
+// back into the bitmap.  Every round reads remote labels as of the previous
+// exchange -- a stale read is re-evaluated through the dirty marks like any
+// other speculation, so the fixpoint is still the sequential sweep.  Heavy
+// vertices are not deferred (a round-local policy would need a global vote).
+void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickless, int round) {
+    DeviceGraph &g = ctx->g;
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = g.n;
+    const KernelSet ks = kernels_for(ctx, cfg, true);
+    const SweepArgs a = make_args(ctx, cfg, pickless);
+    const int64_t nwords = (n + 31) / 32;
+    if (round == 0) {
+        CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
+        CUDA_TRY(cudaMemsetAsync(wb.flag_b.p, 0, (size_t)n, s));
+        CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+        for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
+        if (g.n_giant > 0) {
+            k_iota<<<grid_for(g.n_giant, kThreads), kThreads, 0, s>>>(wb.wl_giant.p, g.n_giant);
+            launch_giant(ctx, ks, a, wb.wl_giant.p, g.n_giant, 1);
+        }
+        launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
+        launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    } else {
+        unsigned long long *cur_lo = wb.counters.p + CNT_LO * CNT_STRIPES,
+                           *cur_mid = wb.counters.p + CNT_MID * CNT_STRIPES,
+                           *cur_hi = wb.counters.p + CNT_HI * CNT_STRIPES,
+                           *cur_giant = wb.counters.p + CNT_GIANT * CNT_STRIPES;
+        CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
+        CUDA_TRY(cudaMemsetAsync(cur_mid, 0, sizeof(unsigned long long), s));
+        CUDA_TRY(cudaMemsetAsync(cur_hi, 0, sizeof(unsigned long long), s));
+        CUDA_TRY(cudaMemsetAsync(cur_giant, 0, sizeof(unsigned long long), s));
+        launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
+        launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_a.p, wb.wl_hi.p, cur_hi);
+        launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_a.p, wb.wl_mid.p, cur_mid);
+        launch_filter(s, g.bin_giant.p, g.n_giant, wb.dirty_a.p, wb.wl_giant.p, cur_giant, 1);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+        read_counters(ctx);
+        const int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
+                      nhi = (int64_t)ctx->h_sum[CNT_HI], ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
+        launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
+        launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
+        launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
+    }
+    giant_join(ctx);
+    if (n > 0) k_dirty_bits_to_bytes<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, wb.dirty_bytes.p, n);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    ctx->stats.rounds += 1;
+}
+
+int64_t slpa_part_det_import_impl(slpa_ctx *ctx) {
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->g.n;
+    wb.dcount.alloc(1);
+    unsigned long long *cnt = wb.dcount.p;
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    if (n > 0) k_dirty_bytes_to_bits<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.dirty_bytes.p, wb.dirty_a.p, n, cnt);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return (int64_t)h;
+}
+
+// End of a partitioned deterministic sweep: the owned changed vertices mark
+// their neighbours t <= v (possibly remote; the host MAX-reduces the flags),
+// L1 is folded into L0 across the whole replica, and the flags produced by
+// this sweep become the current ones.
+int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg) {
+    DeviceGraph &g = ctx->g;
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = g.n;
+    const SweepArgs a = make_args(ctx, cfg, 0);
+    CUDA_TRY(cudaMemsetAsync(wb.counters.p + CNT_DELTA * CNT_STRIPES, 0, CNT_STRIPES * sizeof(unsigned long long), s));
+    if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
+    if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
+    if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
+    if (g.n_giant > 0)
+        k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
+    if (n > 0) k_fold_all<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, wb.lab_new.p, n);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(wb.flag_a.p, wb.flag_b.p, (size_t)n, cudaMemcpyDeviceToDevice, s));
+    read_counters(ctx);
+    ctx->stats.sweeps += 1;
+    return (int64_t)ctx->h_sum[CNT_DELTA];
+}
 
 // ====================================================================== drivers
 int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {

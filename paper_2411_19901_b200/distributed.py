@@ -2,8 +2,8 @@
 one Engine) per GPU, label / mark exchange over torch.distributed (NCCL on
 GPUs; the exchange logic is backend-agnostic and is tested with gloo).
 
-Per sweep (the asynchronous model of the paper's multi-GPU extension,
-SURVEY §8(e)):
+Asynchronous sweeps (worker_count > 0; the paper's multi-GPU model,
+SURVEY §8(e2)), per sweep:
 
 1. every rank sweeps its own rows in place (libslpa_b200 ``slpa_part_sweep``)
    reading its label replica -- remote labels are one exchange old;
@@ -12,6 +12,15 @@ SURVEY §8(e)):
    "neighbour changed" marks of lpa.py:223 for vertices other ranks own;
    ``slpa_part_end_exchange`` then clears the remote entries;
 4. delta (changed vertices) is summed; the convergence test is lpa.py:299.
+
+Deterministic sweeps (worker_count == 0) run the speculative
+rounds of the single-GPU engine across ranks: per round every
+rank evaluates its owned flagged / dirty vertices, then the owned ranges of
+the speculative label words (lab_new, bit 31 = changed) are all-gathered and
+the dirty marks MAX-reduced (as bytes: the OR); the sweep ends when no mark is
+set anywhere.  Stale remote reads are re-evaluated through the marks like any
+other speculation, so labels, delta history and iteration count are
+bit-identical to the sequential reference (lpa.py:204-224).
 
 The collectives operate on zero-copy torch views of the library's device
 buffers (``Engine.part_buffers``); torch is the plumbing, the sweep is the
@@ -98,21 +107,44 @@ def _sync(t):
         torch.cuda.current_stream(t.device).synchronize()
 
 
+def _det_sweep(engine, cfg, pickless, ex, lab_new, dirty) -> int:
+    """One deterministic partitioned sweep: speculative rounds until no rank
+    holds a dirty vertex, then the commit.  Returns the
+    rank-local count of changed owned vertices."""
+    rnd = 0
+    while True:
+        engine.part_det_round(cfg, pickless, rnd)  # returns after its stream drained
+        ex.labels(lab_new)
+        ex.flags(dirty)
+        _sync(lab_new)
+        if engine.part_det_import() == 0:  # global count: identical on every rank
+            break
+        rnd += 1
+    return engine.part_det_commit(cfg)
+
+
 def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) -> PartitionedResult:
     """lpa_run (lpa.py:262-308) over the ranks of `group`; `engine` holds this
-    rank's rows (Engine.part_gen_rmat / part_upload).  cfg.worker_count must
-    be > 0 (the asynchronous sweep)."""
+    rank's rows (Engine.part_gen_rmat / part_upload).  worker_count > 0: the
+    asynchronous partitioned sweep; worker_count == 0: the deterministic one
+    (bit-identical to the sequential reference)."""
     cfg.validate()
     ex = Exchange(ranges, group)
     n = engine.n
     engine.part_begin(cfg)
     lab, fl = engine.part_buffers()
+    det = cfg.worker_count == 0
+    if det:
+        lab_new, dirty = engine.part_det_buffers()
     history = []
     converged = False
     for it in range(cfg.max_iterations):
         pickless = (it % cfg.pickless_gap) == 0
-        local = engine.part_sweep(cfg, pickless)  # returns after its stream drained
-        ex.labels(lab)
+        if det:
+            local = _det_sweep(engine, cfg, pickless, ex, lab_new, dirty)
+        else:
+            local = engine.part_sweep(cfg, pickless)  # returns after its stream drained
+            ex.labels(lab)
         ex.flags(fl)
         _sync(lab)  # collectives on torch's stream finish before the library touches the buffers
         engine.part_end_exchange()

@@ -296,6 +296,31 @@ class Engine:
     def part_end_exchange(self):
         check(self.lib, self.ctx, self.lib.slpa_part_end_exchange(self.ctx))
 
+    # deterministic partitioned sweep (worker_count == 0), one round per call
+    def part_det_round(self, cfg, pickless, rnd):
+        c = config_struct(cfg)
+        check(self.lib, self.ctx, self.lib.slpa_part_det_round(self.ctx, ctypes.byref(c), 1 if pickless else 0,
+                                                               int(rnd)))
+
+    def part_det_import(self) -> int:
+        t = ctypes.c_int64(0)
+        check(self.lib, self.ctx, self.lib.slpa_part_det_import(self.ctx, ctypes.byref(t)))
+        return int(t.value)
+
+    def part_det_commit(self, cfg) -> int:
+        c = config_struct(cfg)
+        ch = ctypes.c_int64(0)
+        check(self.lib, self.ctx, self.lib.slpa_part_det_commit(self.ctx, ctypes.byref(c), ctypes.byref(ch)))
+        return int(ch.value)
+
+    def part_det_buffers(self):
+        """(lab_new, dirty) as zero-copy torch CUDA tensors: the speculative
+        end-of-sweep label words (int32 view of uint32[n], bit 31 = changed)
+        and the dirty marks as bytes (uint8[n])."""
+        lp, dp = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        check(self.lib, self.ctx, self.lib.slpa_part_det_buffers(self.ctx, ctypes.byref(lp), ctypes.byref(dp)))
+        return (device_tensor(lp.value, self.n, "<i4", self.device), device_tensor(dp.value, self.n, "|u1", self.device))
+
     def part_buffers(self):
         """(labels, flags) as zero-copy torch CUDA tensors over the context's
         label replica (int32[n]) and flag array (uint8[n])."""

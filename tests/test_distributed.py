@@ -179,3 +179,150 @@ def test_gpu_two_ranks_one_device(oracle):
                                                partial_groups=32, shared_sketch=False))())
     q_ref = oracle.modularity(g, ref.labels)
     assert q0 >= q_ref - 0.01, (q0, q_ref)
+
+
+# ---------------------------------------------------------------- deterministic partitioned sweep (§8 e3)
+CHG = np.uint32(0x80000000)
+LMASK = np.uint32(0x7FFFFFFF)
+
+
+class MockDetEngine(MockEngine):
+    """CPU stand-in for the deterministic Engine.part_det_* protocol: each
+    round evaluates the owned flagged (round 0) or dirty vertices against the
+    speculative label words (lower neighbours: L1, higher: L0) and marks the
+    higher-positioned dependants of any vertex whose word moves -- the
+    speculative-round scheme of DESIGN.md §3, restated on the CPU."""
+
+    def part_begin(self, cfg):
+        import torch
+        super().part_begin(cfg)
+        self.lab_new = torch.arange(self.n, dtype=torch.int32)
+        self.dirty = torch.zeros(self.n, dtype=torch.uint8)
+        self.fnext = np.zeros(self.n, dtype=np.uint8)
+
+    def part_det_buffers(self):
+        return self.lab_new, self.dirty
+
+    def part_det_round(self, cfg, pickless, rnd):
+        g = self.g
+        L0 = self.lab.numpy()
+        L1 = self.lab_new.numpy().view(np.uint32)
+        F0 = self.fl.numpy()
+        d = self.dirty.numpy()
+        if rnd == 0:
+            self.fnext[:] = 0
+            work = [v for v in range(self.v_begin, self.v_end) if F0[v] and g.degree(v) > 0]
+        else:
+            work = [v for v in range(self.v_begin, self.v_end) if d[v]]
+        marks = np.zeros(self.n, dtype=np.uint8)
+        for v in work:
+            nb = g.targets[g.offsets[v]:g.offsets[v + 1]]
+            view = L0.copy()
+            view[:v] = (L1[:v] & LMASK).astype(np.int32)
+            cand = self.oracle.select(g, view, v, cfg)
+            cur = int(L0[v])
+            lower_changed = bool(np.any((L1[nb[nb < v]] & CHG) != 0))
+            turn = bool(F0[v]) or lower_changed
+            chg = turn and cand != cur and (not pickless or cand < cur)
+            word = np.uint32(cand) | CHG if chg else np.uint32(cur)
+            if word != L1[v]:
+                L1[v] = word
+                marks[nb[nb > v]] = 1
+        d[:] = marks
+
+    def part_det_import(self):
+        return int(self.dirty.numpy().astype(np.int64).sum())
+
+    def part_det_commit(self, cfg):
+        g = self.g
+        L0 = self.lab.numpy()
+        L1 = self.lab_new.numpy().view(np.uint32)
+        delta = 0
+        for v in range(self.v_begin, self.v_end):
+            if L1[v] & CHG:
+                delta += 1
+                nb = g.targets[g.offsets[v]:g.offsets[v + 1]]
+                self.fnext[nb[nb <= v]] = 1
+        moved = (L1 & CHG) != 0
+        L0[moved] = (L1[moved] & LMASK).astype(np.int32)
+        L1[moved] &= LMASK
+        self.fl.numpy()[:] = self.fnext
+        return delta
+
+
+def _det_worker(rank, world, port, payload, out):
+    import torch.distributed as dist
+    from oracle.oracle import HostGraph, get_oracle
+    from paper_2411_19901_b200 import LpaConfig
+    from paper_2411_19901_b200.distributed import lpa_run_partitioned
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = HostGraph(*payload["graph"])
+    cfg = LpaConfig(**payload["cfg"])
+    ranges = payload["ranges"]
+    eng = MockDetEngine(g, ranges[rank][0], ranges[rank][1], get_oracle())
+    res = lpa_run_partitioned(eng, cfg, ranges)
+    out[rank] = (eng.lab.numpy().copy(), res.delta_history, res.converged)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("variant,world", [("mg", 2), ("bm", 2), ("mg", 3)])
+def test_gloo_deterministic_partition_equals_sequential_reference(oracle, variant, world):
+    """The deterministic partitioned protocol reproduces the sequential sweep
+    (the oracle, pinned to the reference's golden vectors) bit for bit."""
+    import torch.multiprocessing as mp
+    from paper_2411_19901_b200 import LpaConfig
+    from paper_2411_19901_b200.distributed import partition_ranges
+    g = oracle.rmat(8, seed=33, permute=True)
+    cfg = LpaConfig(variant=variant, degree_threshold=16, partial_groups=4)
+    ranges = partition_ranges(g.num_vertices, world, np.diff(g.offsets))
+    payload = {"graph": (g.offsets, g.targets, g.weights), "cfg": cfg.__dict__, "ranges": ranges}
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_det_worker, args=(world, _free_port(), payload, out), nprocs=world, join=True)
+    ref = oracle.lpa_run(g, cfg)
+    for r in range(world):
+        lab, hist, conv = out[r]
+        assert hist == ref.delta_history
+        assert conv == ref.converged
+        np.testing.assert_array_equal(lab, ref.labels)
+
+
+def _gpu_det_worker(rank, world, port, scale, variant, out):
+    import torch.distributed as dist
+    import paper_2411_19901_b200 as slpa
+    from paper_2411_19901_b200.distributed import lpa_run_partitioned, partition_ranges
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 1 << scale
+    ranges = partition_ranges(n, world)
+    eng = slpa.Engine(0)
+    eng.part_gen_rmat(scale, *ranges[rank], seed=78, permute=True)
+    cfg = slpa.LpaConfig(variant=variant)
+    res = lpa_run_partitioned(eng, cfg, ranges)
+    lab, _ = eng.part_buffers()
+    out[rank] = (lab.cpu().numpy(), res.delta_history, res.converged, res.iterations)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,world", [("mg", 2), ("bm", 2), ("mg", 3)])
+def test_gpu_deterministic_partition_bit_exact(oracle, variant, world):
+    """Two / three processes share one B200 (gloo over CUDA tensors) and run
+    the CUDA deterministic partitioned sweep: every replica equals the
+    sequential reference (oracle) bit for bit."""
+    import torch.multiprocessing as mp
+    from paper_2411_19901_b200 import LpaConfig
+    scale = 14
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gpu_det_worker, args=(world, _free_port(), scale, variant, out), nprocs=world, join=True)
+    g = oracle.rmat(scale, seed=78, permute=True)
+    ref = oracle.lpa_run(g, LpaConfig(variant=variant))
+    for r in range(world):
+        lab, hist, conv, iters = out[r]
+        assert hist == ref.delta_history
+        assert (iters, conv) == (ref.iterations, ref.converged)
+        np.testing.assert_array_equal(lab, ref.labels)
