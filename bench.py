@@ -333,11 +333,12 @@ def main():
     total_ms = sum(v["ms"] for v in prof.values())
     traffic = None
     tfile = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
+    if os.path.exists(tfile):  # written by tools/ncu_traffic.py from an ncu capture of the same workload
         with open(tfile) as f:
             tj = json.load(f)
-        if tj.get("kernel_class") == dom_name and tj.get("scale") == args.scale and tj.get("variant") == args.variant:
-            traffic = tj.get("dram_bytes_per_launch")
+        if tj.get("scale") == args.scale and tj.get("variant") == args.variant and tj.get("mode") == args.mode:
+            c = tj.get("classes", {}).get(dom_name)
+            traffic = c.get("dram_bytes_per_launch") if c else None
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
