@@ -185,7 +185,12 @@ int32_t slpa_create(int32_t device, slpa_ctx **out) {
             CUDA_TRY(cudaEventCreate(&c->ev1));
             CUDA_TRY(cudaEventCreate(&c->pev0));
             CUDA_TRY(cudaEventCreate(&c->pev1));
-            CUDA_TRY(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+            // giants run on a higher-priority stream: their long sequential
+            // chunk chains must start as soon as SMs free up, not after the
+            // concurrent high-degree scan has drained
+            int prio_lo = 0, prio_hi = 0;
+            CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+            CUDA_TRY(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_hi));
             CUDA_TRY(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
             CUDA_TRY(cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming));
         } catch (...) {

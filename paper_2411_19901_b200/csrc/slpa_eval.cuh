@@ -6,6 +6,15 @@
 #include "slpa_sketch.cuh"
 #include "slpa_internal.cuh"
 
+// minimum resident blocks per SM for the two bulk kernels (register caps; A/B builds)
+#ifndef SLPA_HI_MINB
+#define SLPA_HI_MINB 1
+#endif
+#ifndef SLPA_LO_MINB
+#define SLPA_LO_MINB 1
+#endif
+
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -518,7 +527,7 @@ int stage_mode() {
 // for changed vertices (dependant marks in deterministic mode, neighbour
 // flags in async mode) are done by the whole warp, one changed lane at a
 // time, so they are coalesced instead of 32 divergent row loops.
-template <bool DET>
+template <bool DET, bool LANE_WALK = false>
 __device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t v, int32_t cur, int32_t cand,
                                             bool T, int64_t lo, int64_t deg, unsigned long long &n_delta) {
     const int lane = threadIdx.x & 31;
@@ -536,6 +545,28 @@ __device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t
             n_delta = 1;
             walk = true;
         }
+    }
+    if (LANE_WALK && a.symmetric) {
+        // short rows: every changed lane walks its own row, 8 independent
+        // target loads in flight per step (a warp-cooperative walk would
+        // serialise the changed lanes' rows one round trip each)
+        if (walk) {
+            const int64_t hi = lo + deg;
+            for (int64_t e0 = lo; e0 < hi; e0 += 8) {
+                int32_t t[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) t[j] = e0 + j < hi ? __ldg(&a.tgt[e0 + j]) : -1;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (DET) {
+                        if (t[j] > v) mark_dirty(a.dirty_next, t[j]);
+                    } else if (t[j] >= 0) {
+                        a.flag_cur[t[j]] = 1;
+                    }
+                }
+            }
+        }
+        return;
     }
     unsigned m = __ballot_sync(0xffffffffu, walk);
     while (m) {
@@ -693,7 +724,7 @@ __global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int
 
 // Same evaluation as k_lane_win, every lane streaming its own row directly.
 template <class W, class Pol, bool DET>
-__global__ void __launch_bounds__(kThreads) k_lane_direct(SweepArgs a, const int32_t *__restrict__ list,
+__global__ void __launch_bounds__(kThreads, SLPA_LO_MINB) k_lane_direct(SweepArgs a, const int32_t *__restrict__ list,
                                                           int64_t count, int round0) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int32_t v = -1;
@@ -728,7 +759,7 @@ __global__ void __launch_bounds__(kThreads) k_lane_direct(SweepArgs a, const int
     unsigned long long n_delta = 0;
     const int32_t cand = (go && deg) ? pol.result(cur) : cur;
     const bool T = go && (f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v)));
-    lane_finish<DET>(a, go, v, cur, cand, T, lo, deg, n_delta);
+    lane_finish<DET, true>(a, go, v, cur, cand, T, lo, deg, n_delta);
     warp_count(a.counters, go ? 1ull : 0ull, (unsigned long long)deg, n_delta);
 }
 
@@ -957,7 +988,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const
 constexpr int kLpmWords = 32 * 16;  // 32 parts x (8 keys + 8 values)
 
 template <class W, bool DET, class V>
-__global__ void __launch_bounds__(kThreads) k_mg_hi_scan(SweepArgs a, const int32_t *__restrict__ list,
+__global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs a, const int32_t *__restrict__ list,
                                                          int64_t count, int round0) {
     static_assert(sizeof(V) == 4, "scratch holds 32-bit values");
     const int lane = threadIdx.x & 31;

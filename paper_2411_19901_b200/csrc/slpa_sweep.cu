@@ -19,10 +19,23 @@
 //   * L1 and the changed bit share one 32-bit word (bit 31), so a single
 //     gather of a lower neighbour gives its label and whether it changed.
 // Async mode (worker_count > 0) is the paper's in-place parallel sweep.
+#include <chrono>
 #include <cstdlib>
 #include "slpa_eval.cuh"
 
 namespace {
+
+// Next-round worklists from one pass over the dirty bitmap (1, default) or
+// from passes over every degree bin (0); rounds with more light vertices
+// than kScanSortMin re-derive the degree-ordered list from the bins.
+int scan_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_SCAN");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+constexpr int64_t kScanSortMin = 32768;
 
 // SLPA_TRACE=1: per-round worklist sizes on stderr (diagnostics only).
 int trace_rounds() {
@@ -346,6 +359,56 @@ void launch_filter(cudaStream_t s, const int32_t *bin, int64_t count, const uint
     k_filter_dirty<<<grid_for(count, kThreads), kThreads, 0, s>>>(bin, count, dirty, out, cursor, as_index);
 }
 
+// One pass over the dirty bitmap instead of a pass over every degree bin:
+// thread i takes word i, reads the 32 degree classes of its vertices with one
+// 256-bit load, appends the light ones to the next low-degree worklist
+// (ascending position; one atomic per warp) and moves the heavy ones to the
+// pending bitmap (the deferral of k_defer_dirty).  The caller may still
+// re-derive a degree-ordered low worklist from the bins for large rounds.
+__global__ void __launch_bounds__(kThreads) k_scan_dirty(const uint32_t *__restrict__ dirty,
+                                                         uint32_t *__restrict__ pend,
+                                                         const uint8_t *__restrict__ cls, int64_t nwords,
+                                                         int32_t *__restrict__ out,
+                                                         unsigned long long *__restrict__ cursor) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint32_t w = i < nwords ? __ldcg(&dirty[i]) : 0u;
+    uint32_t lom = 0, hvm = 0;
+    if (w) {
+        uint32_t c[8];
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
+                     : "l"(cls + i * 32));
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t cb = (c[b >> 2] >> ((b & 3) * 8)) & 0xffu;
+            const uint32_t bit = 1u << b;
+            if (w & bit) {
+                if (cb == CLS_LO) lom |= bit;
+                else hvm |= bit;
+            }
+        }
+        if (hvm) atomicOr(&pend[i], hvm);
+    }
+    const int cnt = __popc(lom);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(cursor, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = (int)base + incl - cnt;
+    while (lom) {
+        const int b = __ffs(lom) - 1;
+        lom &= lom - 1;
+        out[pos++] = (int32_t)(i * 32 + b);
+    }
+}
+
 // Multi-GPU deterministic sweep: dirty marks cross ranks as bytes (NCCL has
 // no bitwise-OR reduction; a MAX over 0/1 bytes is the OR).
 __global__ void k_dirty_bits_to_bytes(const uint32_t *__restrict__ bits, uint8_t *__restrict__ bytes, int64_t n) {
@@ -529,7 +592,13 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         CUDA_TRY(cudaMemsetAsync(cur_mid, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_hi, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_giant, 0, sizeof(unsigned long long), s));
-        timed_launch(ctx, SLPA_PROF_COMPACT, 4, [&] {
+        const bool bitmap_scan = defer && scan_mode();
+        timed_launch(ctx, SLPA_PROF_COMPACT, bitmap_scan ? 1 : 4, [&] {
+            if (bitmap_scan) {
+                k_scan_dirty<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, wb.dirty_b.p, g.cls.p,
+                                                                            nwords, wb.wl_lo.p, cur_lo);
+                return;
+            }
             launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
             if (defer) {
                 const int32_t *heavy[3] = {g.bin_hi.p, g.bin_mid.p, g.bin_giant.p};
@@ -545,8 +614,16 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             }
             CUDA_TRY(cudaGetLastError());
         });
-        CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (size_t)nwords * sizeof(uint32_t), s));
         read_counters(ctx);
+        if (bitmap_scan && (int64_t)ctx->h_sum[CNT_LO] > kScanSortMin) {
+            // large round: the degree-ordered worklist keeps the lanes of a warp on similar row lengths
+            CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
+            timed_launch(ctx, SLPA_PROF_COMPACT, 1, [&] {
+                launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
+                CUDA_TRY(cudaGetLastError());
+            });
+        }
+        CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (size_t)nwords * sizeof(uint32_t), s));
         if (first) {
             evals0 = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
             arcs0 = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
@@ -567,9 +644,14 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             nhi = (int64_t)ctx->h_sum[CNT_HI];
             ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
         }
-        if (trace_rounds())
-            fprintf(stderr, "[slpa] sweep round %lld: lo %lld mid %lld hi %lld giant %lld\n", (long long)rounds,
-                    (long long)nlo, (long long)nmid, (long long)nhi, (long long)ngiant);
+        if (trace_rounds()) {
+            static auto t_prev = std::chrono::steady_clock::now();
+            const auto t_now = std::chrono::steady_clock::now();
+            fprintf(stderr, "[slpa] sweep round %lld: lo %lld mid %lld hi %lld giant %lld  (+%.0f us)\n",
+                    (long long)rounds, (long long)nlo, (long long)nmid, (long long)nhi, (long long)ngiant,
+                    std::chrono::duration<double, std::micro>(t_now - t_prev).count());
+            t_prev = t_now;
+        }
         if (nlo == 0 && nmid == 0 && nhi == 0 && ngiant == 0) break;
         pend_any = defer != 0;
         launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);

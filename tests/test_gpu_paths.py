@@ -57,6 +57,7 @@ ENVS = [
     {"SLPA_GIANT": "128"},
     {"SLPA_STREAM": "0", "SLPA_GIANT": "5000"},
     {"SLPA_L2_PERSIST_MB": "40"},
+    {"SLPA_SCAN": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
 ]
