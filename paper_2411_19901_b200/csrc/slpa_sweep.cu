@@ -19,6 +19,7 @@
 //   * L1 and the changed bit share one 32-bit word (bit 31), so a single
 //     gather of a lower neighbour gives its label and whether it changed.
 // Async mode (worker_count > 0) is the paper's in-place parallel sweep.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include "slpa_eval.cuh"
@@ -36,6 +37,30 @@ int scan_mode() {
     return m;
 }
 constexpr int64_t kScanSortMin = 32768;
+
+// Next-sweep flags: 0 (default) push them from the changed rows; 1 pull them
+// when more than 1 / kPullRatio of the non-isolated vertices changed; 2
+// always pull.  (Measured at RMAT s24: push is faster -- rows without a
+// changed neighbour scan to the end.)
+int commit_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_COMMIT");
+        return e ? atoi(e) : 0;
+    }();
+    return m;
+}
+constexpr int64_t kPullRatio = 4;
+
+// Heavy (deferred) vertices run once the light worklist is at most this size
+// (default: 1/256 of the light vertices, >= 1024; measured at RMAT s24 the
+// light tail rounds then overlap the heavy round instead of preceding it).
+int64_t defer_min(int64_t n_light) {
+    static const int64_t m = [] {
+        const char *e = getenv("SLPA_DEFER_MIN");
+        return e ? atoll(e) : -1LL;
+    }();
+    return m >= 0 ? m : std::max<int64_t>(1024, n_light / 256);
+}
 
 // SLPA_TRACE=1: per-round worklist sizes on stderr (diagnostics only).
 int trace_rounds() {
@@ -409,6 +434,73 @@ __global__ void __launch_bounds__(kThreads) k_scan_dirty(const uint32_t *__restr
     }
 }
 
+// Pull form of the next-sweep flags (symmetric graphs): F1[t] = some
+// neighbour u >= t changed this sweep (lpa.py:223 marks every neighbour of a
+// changed u; those at or before u are the ones whose turn has passed).  Each
+// row is scanned only until the first such neighbour (rows keep adjacency
+// order, so no suffix shortcut) -- when a large share of the vertices
+// changed this is a few reads per vertex instead of a byte store per arc of
+// every changed row.
+__global__ void __launch_bounds__(kThreads) k_pull_flags_lo(SweepArgs a, const int32_t *__restrict__ list,
+                                                            int64_t count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int32_t t = __ldg(&list[i]);
+    const int64_t hi = __ldg(&a.off[t + 1]);
+    for (int64_t e = __ldg(&a.off[t]); e < hi; e += 4) {
+        int32_t u[4];
+        bool f = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) u[j] = e + j < hi ? __ldg(&a.tgt[e + j]) : -1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f |= u[j] >= t && (__ldcg(&a.lab_new[u[j]]) >> 31) != 0;
+        if (f) {
+            a.flag_next[t] = 1;
+            return;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_pull_flags_hi(SweepArgs a, const int32_t *__restrict__ list,
+                                                            int64_t count) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= count) return;
+    const int32_t t = __ldg(&list[wid]);
+    const int64_t hi = __ldg(&a.off[t + 1]);
+    for (int64_t e = __ldg(&a.off[t]); e < hi; e += 32) {
+        const int64_t x = e + lane;
+        const int32_t u = x < hi ? __ldg(&a.tgt[x]) : -1;
+        if (__any_sync(0xffffffffu, u >= t && (__ldcg(&a.lab_new[u]) >> 31) != 0)) {
+            if (lane == 0) a.flag_next[t] = 1;
+            return;
+        }
+    }
+}
+
+// Fold L1 into L0 and count the changed vertices (thread per vertex).
+__global__ void __launch_bounds__(kThreads) k_fold_count(SweepArgs a, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long d = 0;
+    if (i < n) {
+        const uint32_t w = a.lab_new[i];
+        if (w & SLPA_CHG) {
+            a.lab_old[i] = (int32_t)(w & SLPA_LMASK);
+            a.lab_new[i] = w & SLPA_LMASK;
+            d = 1;
+        }
+    }
+    warp_count(a.counters, 0, 0, d);
+}
+
+__global__ void __launch_bounds__(kThreads) k_count_changed(const uint32_t *__restrict__ lab_new, int64_t n,
+                                                            unsigned long long *__restrict__ ctr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool c = i < n && (__ldcg(&lab_new[i]) >> 31) != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(ctr, (unsigned long long)__popc(m));
+}
+
 // Multi-GPU deterministic sweep: dirty marks cross ranks as bytes (NCCL has
 // no bitwise-OR reduction; a MAX over 0/1 bytes is the OR).
 __global__ void k_dirty_bits_to_bytes(const uint32_t *__restrict__ bits, uint8_t *__restrict__ bytes, int64_t n) {
@@ -631,7 +723,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         }
         int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
                 nhi = (int64_t)ctx->h_sum[CNT_HI], ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
-        if (defer && nlo == 0 && pend_any) {  // light vertices quiet: run the pending heavy ones
+        if (defer && nlo <= defer_min(g.n_lo) && pend_any) {  // light vertices (nearly) quiet: run the pending heavy ones
             timed_launch(ctx, SLPA_PROF_COMPACT, 3, [&] {
                 launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_b.p, wb.wl_hi.p, cur_hi);
                 launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_b.p, wb.wl_mid.p, cur_mid);
@@ -663,8 +755,32 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     giant_join(ctx);
     const unsigned long long evals = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
     const unsigned long long arcs = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
-    // commit: L0 <- L1, delta, next-sweep flags
-    timed_launch(ctx, SLPA_PROF_COMMIT, 4, [&] {
+    // commit: L0 <- L1, delta, next-sweep flags.  Many changed vertices:
+    // pull the flags (a short suffix scan per vertex); few: push them from the
+    // changed rows.
+    bool pull = false;
+    if (g.symmetric && commit_mode() != 0 && n > 0) {
+        wb.dcount.alloc(1);
+        CUDA_TRY(cudaMemsetAsync(wb.dcount.p, 0, sizeof(unsigned long long), s));
+        k_count_changed<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_new.p, n, wb.dcount.p);
+        unsigned long long nchg = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nchg, wb.dcount.p, sizeof(nchg), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const int64_t active = g.n_lo + g.n_mid + g.n_hi + g.n_giant;
+        pull = commit_mode() == 2 || (int64_t)nchg * kPullRatio > active;
+    }
+    if (pull) {
+        timed_launch(ctx, SLPA_PROF_COMMIT, 5, [&] {
+            if (g.n_lo > 0) k_pull_flags_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
+            const int32_t *heavy[3] = {g.bin_mid.p, g.bin_hi.p, g.bin_giant.p};
+            const int64_t nheavy[3] = {g.n_mid, g.n_hi, g.n_giant};
+            for (int h = 0; h < 3; ++h)
+                if (nheavy[h] > 0)
+                    k_pull_flags_hi<<<grid_for(nheavy[h] * 32, kThreads), kThreads, 0, s>>>(a, heavy[h], nheavy[h]);
+            k_fold_count<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, n);
+            CUDA_TRY(cudaGetLastError());
+        });
+    } else timed_launch(ctx, SLPA_PROF_COMMIT, 4, [&] {
         if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
         if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
         if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);

@@ -58,6 +58,10 @@ ENVS = [
     {"SLPA_STREAM": "0", "SLPA_GIANT": "5000"},
     {"SLPA_L2_PERSIST_MB": "40"},
     {"SLPA_SCAN": "0", "SLPA_GIANT": "300"},
+    {"SLPA_COMMIT": "0", "SLPA_GIANT": "300"},
+    {"SLPA_COMMIT": "2", "SLPA_GIANT": "300"},
+    {"SLPA_DEFER_MIN": "0", "SLPA_GIANT": "300"},
+    {"SLPA_DEFER_MIN": "50", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
 ]
