@@ -108,6 +108,10 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.flag_b.alloc(n);
     wb.dirty_a.alloc(n / 32 + 1);
     wb.dirty_b.alloc(n / 32 + 1);
+    if (ctx->g.n_giant > 0) {
+        wb.dirty_g.alloc(n / 32 + 1);
+        wb.dirty_gp.alloc(n / 32 + 1);
+    }
     wb.wl_lo.alloc(n);
     wb.wl_mid.alloc(n);
     wb.wl_hi.alloc(n);

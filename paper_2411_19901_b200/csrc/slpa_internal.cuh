@@ -97,7 +97,7 @@ struct SweepArgs {
     uint2 *hmeta;                     //   (cur label, active | f0 << 1 | lower_changed << 2) per entry
 };
 
-enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_GIANT = 8, CNT_N = 9 };
+enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_GIANT = 8, CNT_GPEND = 9, CNT_N = 10 };
 #define CNT_STRIPES 64
 #define CNT_TOTAL (CNT_N * CNT_STRIPES)
 
@@ -147,6 +147,7 @@ struct WorkBuffers {
     DevBuf<uint32_t> lab_new;
     DevBuf<uint8_t> flag_a, flag_b;
     DevBuf<uint32_t> dirty_a, dirty_b;
+    DevBuf<uint32_t> dirty_g, dirty_gp;  // asynchronous giants: their marks / marks waiting for them
     DevBuf<uint8_t> dirty_bytes;  // multi-GPU deterministic: dirty marks exchanged as bytes
     DevBuf<unsigned long long> dcount;
     DevBuf<int32_t> wl_lo, wl_mid, wl_hi, wl_giant;
@@ -161,7 +162,7 @@ struct WorkBuffers {
     DevBuf<unsigned long long> metric_u;
     DevBuf<unsigned char> scratch;  // cub temp storage
     size_t bytes() const {
-        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() +
+        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() + dirty_g.bytes() + dirty_gp.bytes() +
                dirty_b.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
     }

@@ -38,6 +38,16 @@ int scan_mode() {
 }
 constexpr int64_t kScanSortMin = 32768;
 
+// Giants run asynchronously across rounds (1, default) or are joined every
+// round (0).
+int giant_async_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_GIANT_ASYNC");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
 // Next-sweep flags: 0 (default) push them from the changed rows; 1 pull them
 // when more than 1 / kPullRatio of the non-isolated vertices changed; 2
 // always pull.  (Measured at RMAT s24: push is faster -- rows without a
@@ -394,11 +404,13 @@ __global__ void __launch_bounds__(kThreads) k_scan_dirty(const uint32_t *__restr
                                                          uint32_t *__restrict__ pend,
                                                          const uint8_t *__restrict__ cls, int64_t nwords,
                                                          int32_t *__restrict__ out,
-                                                         unsigned long long *__restrict__ cursor) {
+                                                         unsigned long long *__restrict__ cursor,
+                                                         uint32_t *__restrict__ pend_g,
+                                                         unsigned long long *__restrict__ new_g) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint32_t w = i < nwords ? __ldcg(&dirty[i]) : 0u;
-    uint32_t lom = 0, hvm = 0;
+    uint32_t lom = 0, hvm = 0, gm = 0;
     if (w) {
         uint32_t c[8];
         asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -410,10 +422,15 @@ __global__ void __launch_bounds__(kThreads) k_scan_dirty(const uint32_t *__restr
             const uint32_t bit = 1u << b;
             if (w & bit) {
                 if (cb == CLS_LO) lom |= bit;
+                else if (cb == CLS_GIANT && pend_g) gm |= bit;
                 else hvm |= bit;
             }
         }
         if (hvm) atomicOr(&pend[i], hvm);
+        if (gm) {  // asynchronous giants: their own pending set, counted when new
+            const uint32_t old = atomicOr(&pend_g[i], gm);
+            if (gm & ~old) atomicAdd(new_g, (unsigned long long)__popc(gm & ~old));
+        }
     }
     const int cnt = __popc(lom);
     int incl = cnt;
@@ -499,6 +516,26 @@ __global__ void __launch_bounds__(kThreads) k_count_changed(const uint32_t *__re
     const bool c = i < n && (__ldcg(&lab_new[i]) >> 31) != 0;
     const unsigned m = __ballot_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(ctr, (unsigned long long)__popc(m));
+}
+
+// Asynchronous giants: OR a finished batch's dependant marks into the round
+// bitmap and clear them; move a class's round-0 deferral bits to its own set.
+__global__ void k_or_clear(uint32_t *__restrict__ src, uint32_t *__restrict__ dst, int64_t nwords) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nwords) return;
+    const uint32_t w = src[i];
+    if (w) {
+        atomicOr(&dst[i], w);
+        src[i] = 0;
+    }
+}
+__global__ void k_move_class(const int32_t *__restrict__ bin, int64_t count, uint32_t *__restrict__ from,
+                             uint32_t *__restrict__ to) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int32_t v = __ldg(&bin[i]);
+    const uint32_t bit = 1u << (v & 31);
+    if (atomicAnd(&from[v >> 5], ~bit) & bit) atomicOr(&to[v >> 5], bit);
 }
 
 // Multi-GPU deterministic sweep: dirty marks cross ranks as bytes (NCCL has
@@ -678,8 +715,38 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
                        *cur_hi = wb.counters.p + CNT_HI * CNT_STRIPES,
                        *cur_giant = wb.counters.p + CNT_GIANT * CNT_STRIPES;
     bool pend_any = defer != 0;
+    // Asynchronous giants (default with deferral and the bitmap scan): a giant
+    // batch runs on the priority stream while the rounds go on; its dependant
+    // marks go to dirty_g and are OR-ed into the round bitmap once the batch
+    // has finished, marks for giants wait in dirty_gp, and at most one batch
+    // is in flight (its gather buffer).  A giant that read a label which
+    // changed later is marked by that change like any other vertex, so the
+    // fixpoint -- the sequential sweep -- is unchanged; the rounds just no
+    // longer wait for the giants' long chunk chains.
+    const bool agiant = defer >= 2 && scan_mode() && g.n_giant > 0 && !ctx->prof_on && giant_async_mode();
+    bool g_inflight = false;
+    int64_t g_pending = 0;
+    SweepArgs ag = a;
+    if (agiant) {
+        ag.dirty_next = wb.dirty_g.p;
+        CUDA_TRY(cudaMemsetAsync(wb.dirty_g.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+        CUDA_TRY(cudaMemsetAsync(wb.dirty_gp.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+        g_pending = g.n_giant;  // round 0: flagged giants sit in dirty_b, moved below
+        k_move_class<<<grid_for(g.n_giant, kThreads), kThreads, 0, s>>>(g.bin_giant.p, g.n_giant, wb.dirty_b.p,
+                                                                       wb.dirty_gp.p);
+        CUDA_TRY(cudaGetLastError());
+    }
     for (;;) {
-        giant_join(ctx);
+        if (agiant) {
+            if (g_inflight && cudaEventQuery(ctx->gev1) == cudaSuccess) {
+                k_or_clear<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_g.p, wb.dirty_a.p, nwords);
+                CUDA_TRY(cudaGetLastError());
+                g_inflight = false;
+                ctx->giant_pending = 0;
+            }
+        } else {
+            giant_join(ctx);
+        }
         CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_mid, 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaMemsetAsync(cur_hi, 0, sizeof(unsigned long long), s));
@@ -687,8 +754,9 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         const bool bitmap_scan = defer && scan_mode();
         timed_launch(ctx, SLPA_PROF_COMPACT, bitmap_scan ? 1 : 4, [&] {
             if (bitmap_scan) {
-                k_scan_dirty<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, wb.dirty_b.p, g.cls.p,
-                                                                            nwords, wb.wl_lo.p, cur_lo);
+                k_scan_dirty<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(
+                    wb.dirty_a.p, wb.dirty_b.p, g.cls.p, nwords, wb.wl_lo.p, cur_lo, agiant ? wb.dirty_gp.p : nullptr,
+                    wb.counters.p + CNT_GPEND * CNT_STRIPES);
                 return;
             }
             launch_filter(s, g.bin_lo.p, g.n_lo, wb.dirty_a.p, wb.wl_lo.p, cur_lo);
@@ -723,14 +791,25 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         }
         int64_t nlo = (int64_t)ctx->h_sum[CNT_LO], nmid = (int64_t)ctx->h_sum[CNT_MID],
                 nhi = (int64_t)ctx->h_sum[CNT_HI], ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
-        if (defer && nlo <= defer_min(g.n_lo) && pend_any) {  // light vertices (nearly) quiet: run the pending heavy ones
+        if (agiant) g_pending += (int64_t)ctx->h_sum[CNT_GPEND];
+        CUDA_TRY(cudaMemsetAsync(wb.counters.p + CNT_GPEND * CNT_STRIPES, 0, sizeof(unsigned long long), s));
+        const bool quiet = nlo <= defer_min(g.n_lo);
+        const bool launch_g = agiant && quiet && !g_inflight && g_pending > 0;
+        if (defer && quiet && (pend_any || launch_g)) {  // light vertices (nearly) quiet: run the pending heavy ones
             timed_launch(ctx, SLPA_PROF_COMPACT, 3, [&] {
-                launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_b.p, wb.wl_hi.p, cur_hi);
-                launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_b.p, wb.wl_mid.p, cur_mid);
-                launch_filter(s, g.bin_giant.p, g.n_giant, wb.dirty_b.p, wb.wl_giant.p, cur_giant, 1);
+                if (pend_any) {
+                    launch_filter(s, g.bin_hi.p, g.n_hi, wb.dirty_b.p, wb.wl_hi.p, cur_hi);
+                    launch_filter(s, g.bin_mid.p, g.n_mid, wb.dirty_b.p, wb.wl_mid.p, cur_mid);
+                    if (!agiant) launch_filter(s, g.bin_giant.p, g.n_giant, wb.dirty_b.p, wb.wl_giant.p, cur_giant, 1);
+                }
+                if (launch_g) launch_filter(s, g.bin_giant.p, g.n_giant, wb.dirty_gp.p, wb.wl_giant.p, cur_giant, 1);
                 CUDA_TRY(cudaGetLastError());
             });
-            CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+            if (pend_any) CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+            if (launch_g) {
+                CUDA_TRY(cudaMemsetAsync(wb.dirty_gp.p, 0, (size_t)nwords * sizeof(uint32_t), s));
+                g_pending = 0;
+            }
             read_counters(ctx);
             nmid = (int64_t)ctx->h_sum[CNT_MID];
             nhi = (int64_t)ctx->h_sum[CNT_HI];
@@ -744,9 +823,27 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
                     std::chrono::duration<double, std::micro>(t_now - t_prev).count());
             t_prev = t_now;
         }
-        if (nlo == 0 && nmid == 0 && nhi == 0 && ngiant == 0) break;
+        if (nlo == 0 && nmid == 0 && nhi == 0 && ngiant == 0) {
+            if (!agiant || (!g_inflight && g_pending == 0)) break;
+            if (g_inflight) {  // only the giant batch is left: wait for it, merge its marks
+                CUDA_TRY(cudaEventSynchronize(ctx->gev1));
+                k_or_clear<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_g.p, wb.dirty_a.p, nwords);
+                CUDA_TRY(cudaGetLastError());
+                g_inflight = false;
+                ctx->giant_pending = 0;
+            }
+            pend_any = true;  // the merged marks may include deferred heavy vertices
+            continue;
+        }
         pend_any = defer != 0;
-        launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
+        if (agiant) {
+            if (ngiant > 0) {
+                launch_giant(ctx, ks, ag, wb.wl_giant.p, ngiant, 0);
+                g_inflight = true;
+            }
+        } else {
+            launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
+        }
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
         launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
         launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);

@@ -62,6 +62,8 @@ ENVS = [
     {"SLPA_COMMIT": "2", "SLPA_GIANT": "300"},
     {"SLPA_DEFER_MIN": "0", "SLPA_GIANT": "300"},
     {"SLPA_DEFER_MIN": "50", "SLPA_GIANT": "300"},
+    {"SLPA_GIANT_ASYNC": "0", "SLPA_GIANT": "300"},
+    {"SLPA_GIANT": "1000", "SLPA_HI_SPLIT": "300"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
 ]

@@ -3,6 +3,7 @@ timeout 900 python -m pytest tests/test_gpu_paths.py tests/test_gpu_parity.py te
 run() { echo "=== $*"; env "$@" timeout 300 python tools/prof_run.py --scale 24 --runs 4 | tail -1; }
 {
 run SLPA_X=0
-echo "=== async"; timeout 300 python tools/prof_run.py --scale 24 --runs 3 --mode async | tail -1
+run SLPA_GIANT_ASYNC=0
+run SLPA_X=0
 } > gpurun_out/ab.log 2>&1
 SLPA_TRACE=1 timeout 300 python tools/prof_run.py --scale 24 --runs 3 > gpurun_out/trace_rt.log 2>&1
