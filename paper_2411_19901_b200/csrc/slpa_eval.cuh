@@ -18,6 +18,7 @@
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kGiantWarps = 8;  // block-per-vertex kernels: 8 warps x 4 groups = 32 chunks
 
 // ------------------------------------------------------------------ label reads
 // Deterministic mode: neighbour t of v (positions).  Lower neighbours give
@@ -1084,6 +1085,197 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_finish(SweepArgs a, const in
     warp_hi_finish<DET>(a, v, (int32_t)meta.x, cand, (meta.y & 2u) ? 1 : 0, (meta.y & 4u) != 0, lo, hi, lane);
 }
 
+// Group-wise chunk scan straight from the CSR: the 8 lanes of a group hold
+// the 8 slots of one part sketch; lane sl loads arc x + sl of each batch
+// (32-byte coalesced per group) and gathers its label, DEPTH batches ahead,
+// then every arc is broadcast to the group and accumulated slot-parallel
+// (first matching lane, else first empty lane, else every lane decrements).
+// The per-arc chain is a few instructions and one vote -- ~5x shorter than a
+// lane's register-sketch update -- which is what long chunks need.
+template <class W, bool DET, class V>
+__device__ __forceinline__ void group_chunk_scan(const SweepArgs &a, int64_t start, int64_t len, int64_t maxlen,
+                                                 int32_t v, int sl, int gb, int32_t &key, V &val, bool &lc) {
+    constexpr int D = 4;  // batches in flight
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    uint32_t Lr[D];
+    W wr[D];
+    auto fetch = [&](int64_t x, uint32_t &L, W &w) {
+        L = 0;
+        w = (W)0;
+        if (x + sl < len) {
+            const int32_t t = __ldg(&a.tgt[start + x + sl]);
+            if (t != v) {
+                w = __ldg(&wts[start + x + sl]);
+                L = DET ? __ldcg(&a.lab_new[t]) : (uint32_t)__ldcg(&a.lab_old[t]);
+                if (DET && t > v && (L >> 31)) L = (uint32_t)__ldg(&a.lab_old[t]);
+            }
+        }
+    };
+#pragma unroll
+    for (int d = 0; d < D; ++d) fetch((int64_t)d * 8, Lr[d], wr[d]);
+    for (int64_t x0 = 0; x0 < maxlen; x0 += 8 * D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int64_t x = x0 + d * 8;
+            if (x < maxlen) {  // warp-uniform
+                const uint32_t Lx = Lr[d];
+                const W wx = wr[d];
+                fetch(x + 8 * D, Lr[d], wr[d]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t Lj = __shfl_sync(0xffffffffu, Lx, gb + j);
+                    const W wj = __shfl_sync(0xffffffffu, wx, gb + j);
+                    const bool live = x + j < len && wj != (W)0;  // group-uniform
+                    lc |= live && (Lj >> 31) != 0;
+                    const int32_t c = (int32_t)(Lj & SLPA_LMASK);
+                    const V w = (V)wj;
+                    const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c)) >> gb) & 0xffu;
+                    const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
+                    const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
+                    const V d0 = (mm | fm) ? (V)0 : w;
+                    if (live) {
+                        const bool mine = (sel >> sl) & 1u;
+                        if (mine) key = c;
+                        val = mine ? val + w : val - (val < d0 ? val : d0);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// High degree, small rounds, fully fused: a block per vertex scans its 32
+// chunks slot-parallel straight from the CSR (group_chunk_scan), stages the
+// part sketches in shared memory, and warp 0 replays them in order on the
+// slot-parallel warp sketch and finishes the vertex -- one launch and short
+// chains, for rounds whose cost is latency rather than volume.
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kGiantWarps * 32) k_mg_hi_block(SweepArgs a, const int32_t *__restrict__ list,
+                                                                 int64_t count, int round0) {
+    __shared__ int32_t s_key[32][8];
+    __shared__ V s_val[32][8];
+    const int64_t idx = blockIdx.x;
+    if (idx >= count) return;
+    const int32_t v = __ldg(&list[idx]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET ? (round0 && !f0) : !f0) return;  // block-uniform
+    if (!DET) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.flag_cur[v] = 0;
+    }
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int grp = lane >> 3, sl = lane & 7, gb = grp * 8;
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t deg = hi - lo;
+    const int P = a.parts;
+    const int p = wib * 4 + grp;
+    int64_t cs = 0, ce = 0;
+    if (p < P) chunk_bounds(deg, P, p, cs, ce);
+    int64_t maxlen = ce - cs;
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+        const int64_t x = __shfl_xor_sync(0xffffffffu, maxlen, o);
+        maxlen = x > maxlen ? x : maxlen;
+    }
+    int32_t key = kNoKey;
+    V val = (V)0;
+    bool lc = false;
+    group_chunk_scan<W, DET, V>(a, lo + cs, ce - cs, maxlen, v, sl, gb, key, val, lc);
+    if (p < P) {
+        s_key[p][sl] = key;
+        s_val[p][sl] = val;
+    }
+    const int lc_any = __syncthreads_or(lc ? 1 : 0);
+    if (wib != 0) return;
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    WarpSketch<V> S_{kNoKey, (V)0};
+    if (lane < 8) {
+        S_.key = s_key[0][lane];
+        S_.val = s_val[0][lane];
+    }
+    for (int q = 1; q < P; ++q) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const V w = s_val[q][i];
+            if (w > (V)0) S_.acc(lane, 8, s_key[q][i], w);
+        }
+    }
+    int32_t best;
+    const bool found = S_.max_key(lane, 8, best);
+    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lc_any != 0, lo, hi, lane);
+}
+
+// Low degree, small rounds: a warp per vertex.  The row's targets, weights
+// and labels are loaded by all lanes at once (one round trip instead of a
+// lane's chain of batches); then the arcs are replayed in adjacency order on
+// the slot-parallel warp sketch (MG, physical slot rules) or on a vote every
+// lane keeps redundantly (BM).  Same results as k_lane_direct; chosen when a
+// round has few light vertices and its cost is latency.
+template <class W, bool DET, class V, bool BM>
+__global__ void __launch_bounds__(kThreads) k_lo_warp(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                      int round0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= count) return;  // warp-uniform
+    const int32_t v = __ldg(&list[wid]);
+    const uint8_t f0 = a.flag_cur[v];
+    if (DET ? (round0 && !f0) : !f0) return;
+    if (!DET) {
+        __syncwarp();
+        if (lane == 0) a.flag_cur[v] = 0;
+    }
+    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+    const int k = a.k;
+    WarpSketch<V> S_{kNoKey, (V)0};
+    BmVote<V> st{cur, (V)0};
+    bool lc = false;
+    for (int pass = 0; pass < (!BM && a.scan_double ? 2 : 1); ++pass) {
+        if (pass == 1) S_.val = (V)0;  // double scan: exact re-count over the physical keys
+        for (int64_t base = lo; base < hi; base += 128) {
+            uint32_t L[4];
+            W w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t e = base + j * 32 + lane;
+                L[j] = 0;
+                w[j] = (W)0;
+                if (e < hi) {
+                    const int32_t t = __ldg(&a.tgt[e]);
+                    if (t != v) {
+                        w[j] = __ldg(&wts[e]);
+                        L[j] = DET ? __ldcg(&a.lab_new[t]) : (uint32_t)__ldcg(&a.lab_old[t]);
+                        if (DET && t > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t]);
+                        if (DET) lc |= (L[j] >> 31) != 0;
+                    }
+                }
+            }
+            const int64_t rem = hi - base;
+            const int nj = rem >= 128 ? 4 : (int)((rem + 31) / 32);
+            for (int j = 0; j < nj; ++j) {
+                const int ns = (int)min((int64_t)32, rem - j * 32);
+                for (int src = 0; src < ns; ++src) {
+                    const W wj = __shfl_sync(0xffffffffu, w[j], src);
+                    const int32_t c = (int32_t)(__shfl_sync(0xffffffffu, L[j], src) & SLPA_LMASK);
+                    if (wj == (W)0) continue;  // self arc (weights are > 0); warp-uniform
+                    if (BM) st.acc(c, (V)wj);
+                    else if (pass == 0) S_.acc(lane, k, c, (V)wj);
+                    else S_.rescan_add(lane, k, c, (V)wj);
+                }
+            }
+        }
+    }
+    int32_t cand = cur;
+    if (BM) {
+        if (hi > lo) cand = st.cand;
+    } else {
+        int32_t best;
+        if (S_.max_key(lane, k, best)) cand = best;
+    }
+    warp_hi_finish<DET>(a, v, cur, cand, f0, __any_sync(0xffffffffu, lc), lo, hi, lane);
+}
+
 // High degree, BM, direct streaming.
 template <class W, bool DET, class V>
 __global__ void __launch_bounds__(kThreads) k_bm_hi_direct(SweepArgs a, const int32_t *__restrict__ list,
@@ -1412,8 +1604,6 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_giant(SweepArgs a, const int
 // lane decrements) instead of a lane's full register-sketch update: the
 // per-chunk sequential chain -- the critical path of a giant -- gets ~5x
 // shorter.  Then warp 0 replays parts 1.. into parts[0] in order.
-constexpr int kGiantWarps = 8;
-
 template <class W, bool DET, class V>
 __global__ void __launch_bounds__(kGiantWarps * 32) k_mg_giant_grp(SweepArgs a, const int32_t *__restrict__ slots,
                                                                   int64_t count, int round0) {
@@ -1629,32 +1819,38 @@ int giant_grp_mode() {
 template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
     if (cfg->variant == SLPA_VARIANT_EXACT)
-        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0, 0, nullptr, nullptr};
+        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0, 0, nullptr, nullptr, nullptr};
     const bool direct = stage_mode() != 0;
     if (cfg->variant == SLPA_VARIANT_BM) {
-        if (direct)
-            return {k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
-                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1, 0, nullptr, nullptr};
+        if (direct) {
+            KernelSet ks{k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
+                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1, 0, nullptr, nullptr, nullptr};
+            ks.lo_small = k_lo_warp<W, DET, V, true>;
+            return ks;
+        }
         return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
-                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1, 0, nullptr, nullptr};
+                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1, 0, nullptr, nullptr, nullptr};
     }
     if (cfg->sketch_slots != 8) {
-        if (direct)
-            return {k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
+        if (direct) {
+            KernelSet ks{k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
                     k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads,
-                    kThreads, 1, 0, nullptr, nullptr};
+                    kThreads, 1, 0, nullptr, nullptr, nullptr};
+            if (cfg->sketch_slots <= SLPA_KHI_MAX) ks.lo_small = k_lo_warp<W, DET, V, false>;
+            return ks;
+        }
         return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
                 k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads,
-                kWinThreads, 1, 0, nullptr, nullptr};
+                kWinThreads, 1, 0, nullptr, nullptr, nullptr};
     }
     if (!direct)
         return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
                 k_mg_hi_win<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kWinThreads,
-                kWinThreads, 1, 0, nullptr, nullptr};
+                kWinThreads, 1, 0, nullptr, nullptr, nullptr};
     const bool grouped_ok = cfg->partial_groups <= 32 && cfg->scan_mode != SLPA_SCAN_DOUBLE;
     KernelSet ks{k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
                  k_mg_hi_direct<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads, kThreads,
-                 1, 0, nullptr, nullptr};
+                 1, 0, nullptr, nullptr, nullptr};
     if constexpr (sizeof(V) == 4) {
         if (grouped_ok && hi_grp_mode() == 1) {
             ks.hi = k_mg_hi_grp<W, DET, V>;
@@ -1663,11 +1859,13 @@ KernelSet pick_kernels(const slpa_config *cfg) {
         } else if (grouped_ok && hi_grp_mode() == 2) {
             if (DET) {  // async keeps the fused kernel: labels move within the launch
                 ks.hi = k_mg_hi_scan<W, DET, V>;
+                ks.hi_small = k_mg_hi_block<W, DET, V>;
                 ks.hi_merge = k_mg_hi_merge<W, DET, V>;
                 ks.hi_finish = k_mg_hi_finish<DET>;
             }
         }
     }
+    ks.lo_small = k_lo_warp<W, DET, V, false>;
     if (grouped_ok && giant_grp_mode()) {
         ks.giant = k_mg_giant_grp<W, DET, V>;
         ks.giant_threads = kGiantWarps * 32;

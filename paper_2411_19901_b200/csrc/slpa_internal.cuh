@@ -203,6 +203,8 @@ struct KernelSet {
     int giant_threads;  // giant kernel: block per giant of this size (0 = warp per giant)
     EvalKernel hi_merge;   // non-null: `hi` is a scan writing part sketches, this kernel merges them
     EvalKernel hi_finish;  //   and this one (a warp per vertex) commits the merged candidates
+    EvalKernel hi_small;   // small high-degree rounds: fused block-per-vertex kernel
+    EvalKernel lo_small;   // small low-degree rounds: warp per vertex
 };
 
 // slpa_eval_<weights>_<sketch values>_<mode>.cu

@@ -21,6 +21,7 @@
 // Async mode (worker_count > 0) is the paper's in-place parallel sweep.
 #include <algorithm>
 #include <chrono>
+#include <vector>
 #include <cstdlib>
 #include "slpa_eval.cuh"
 
@@ -37,6 +38,26 @@ int scan_mode() {
     return m;
 }
 constexpr int64_t kScanSortMin = 32768;
+
+// High-degree rounds with at most this many vertices use the block-per-vertex
+// slot-parallel scan (short chains) instead of the warp-per-vertex one.
+int64_t hi_small_max() {
+    static const int64_t m = [] {
+        const char *e = getenv("SLPA_HI_SMALL");
+        return e ? atoll(e) : 16384LL;
+    }();
+    return m;
+}
+
+// Low-degree rounds with at most this many vertices use the warp-per-vertex
+// kernel.
+int64_t lo_small_max() {
+    static const int64_t m = [] {
+        const char *e = getenv("SLPA_LO_SMALL");
+        return e ? atoll(e) : 2048LL;
+    }();
+    return m;
+}
 
 // Giants run asynchronously across rounds (1, default) or are joined every
 // round (0).
@@ -73,6 +94,16 @@ int64_t defer_min(int64_t n_light) {
 }
 
 // SLPA_TRACE=1: per-round worklist sizes on stderr (diagnostics only).
+struct TimelineEv {
+    int cls;
+    bool giant;
+    cudaEvent_t e0, e1;
+};
+std::vector<TimelineEv> &timeline() {
+    static std::vector<TimelineEv> t;
+    return t;
+}
+
 int trace_rounds() {
     static const int t = [] {
         const char *e = getenv("SLPA_TRACE");
@@ -297,9 +328,22 @@ void read_counters(slpa_ctx *ctx) {
 // around every launch, attributed to a kernel class with the vertices and
 // arcs that launch evaluated.  Off by default (no host syncs added).
 template <class F>
-void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn) {
+void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn, cudaStream_t st = nullptr) {
     ctx->stats.kernel_launches += nlaunch;
     if (!ctx->prof_on) {
+        if (trace_rounds() >= 3) {  // timeline: events around the launch, read at the end of the sweep
+            cudaStream_t es = st ? st : ctx->stream;
+            TimelineEv ev;
+            ev.cls = cls;
+            CUDA_TRY(cudaEventCreate(&ev.e0));
+            CUDA_TRY(cudaEventCreate(&ev.e1));
+            CUDA_TRY(cudaEventRecord(ev.e0, es));
+            fn();
+            CUDA_TRY(cudaEventRecord(ev.e1, es));
+            ev.giant = st != nullptr && st != ctx->stream;
+            timeline().push_back(ev);
+            return;
+        }
         fn();
         return;
     }
@@ -323,8 +367,15 @@ void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn) {
 }
 
 void launch_lane(slpa_ctx *ctx, EvalKernel k, int threads, const SweepArgs &a, const int32_t *list, int64_t cnt,
-                 int round0, int cls) {
+                 int round0, int cls, EvalKernel small = nullptr) {
     if (cnt <= 0) return;
+    if (small && cnt <= lo_small_max()) {  // few vertices: a warp per vertex (latency, not volume)
+        timed_launch(ctx, cls, 1, [&] {
+            small<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+            CUDA_TRY(cudaGetLastError());
+        });
+        return;
+    }
     timed_launch(ctx, cls, 1, [&] {
         k<<<grid_for(cnt, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
         CUDA_TRY(cudaGetLastError());
@@ -345,6 +396,11 @@ void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int
     }
     timed_launch(ctx, cls, ks.hi_merge ? 3 : 1, [&] {
         const int64_t items = ks.hi_vpw ? (cnt + ks.hi_vpw - 1) / ks.hi_vpw * 32 : cnt;
+        if (ks.hi_small && cnt <= hi_small_max()) {  // fused block-per-vertex kernel (merge + finish inside)
+            ks.hi_small<<<(unsigned)cnt, kGiantWarps * 32, 0, ctx->stream>>>(aa, list, cnt, round0);
+            CUDA_TRY(cudaGetLastError());
+            return;
+        }
         ks.hi<<<grid_for(items, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(aa, list, cnt, round0);
         if (ks.hi_merge) {
             ks.hi_merge<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(aa, list, cnt, round0);
@@ -374,7 +430,7 @@ void launch_giant(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const 
         else
             ks.giant<<<grid_for(cnt * 32, kWinThreads), kWinThreads, 0, gs>>>(a, slots, cnt, round0);
         CUDA_TRY(cudaGetLastError());
-    });
+    }, gs);
     if (overlap) {
         CUDA_TRY(cudaEventRecord(ctx->gev1, gs));
         ctx->giant_pending = 1;
@@ -623,7 +679,7 @@ void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickles
                       nhi = (int64_t)ctx->h_sum[CNT_HI], ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
         launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK, ks.lo_small);
         launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
     }
     giant_join(ctx);
@@ -845,7 +901,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
         }
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK);
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK, ks.lo_small);
         launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
         ++rounds;
     }
@@ -886,6 +942,24 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         CUDA_TRY(cudaGetLastError());
     });
     read_counters(ctx);
+    if (trace_rounds() >= 3 && !timeline().empty()) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        const char *names[] = {"lo0", "mid0", "hi0", "lo", "mid", "hi", "compact", "commit", "other", "giant"};
+        cudaEvent_t base = timeline().front().e0;
+        for (const TimelineEv &ev : timeline()) {
+            float t0 = 0.f, t1 = 0.f;
+            cudaEventElapsedTime(&t0, base, ev.e0);
+            cudaEventElapsedTime(&t1, base, ev.e1);
+            fprintf(stderr, "[slpa] tl %-8s %s %9.1f %9.1f %8.1f\n", ev.cls >= 0 && ev.cls < 10 ? names[ev.cls] : "?",
+                    ev.giant ? "G" : "M", 1000.f * t0, 1000.f * t1, 1000.f * (t1 - t0));
+        }
+        for (const TimelineEv &ev : timeline()) {
+            cudaEventDestroy(ev.e0);
+            cudaEventDestroy(ev.e1);
+        }
+        timeline().clear();
+        cudaGetLastError();
+    }
     std::swap(wb.flag_a, wb.flag_b);
     ctx->stats.rounds += rounds;
     ctx->stats.vertex_evals += (int64_t)evals;

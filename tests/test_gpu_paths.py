@@ -63,6 +63,10 @@ ENVS = [
     {"SLPA_DEFER_MIN": "0", "SLPA_GIANT": "300"},
     {"SLPA_DEFER_MIN": "50", "SLPA_GIANT": "300"},
     {"SLPA_GIANT_ASYNC": "0", "SLPA_GIANT": "300"},
+    {"SLPA_HI_SMALL": "0", "SLPA_GIANT": "300"},
+    {"SLPA_HI_SMALL": "100000000"},
+    {"SLPA_LO_SMALL": "0"},
+    {"SLPA_LO_SMALL": "100000000", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "1000", "SLPA_HI_SPLIT": "300"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
     {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
