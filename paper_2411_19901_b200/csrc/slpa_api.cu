@@ -1,6 +1,7 @@
 // slpa_api.cu -- the extern "C" boundary (include/slpa.h) and the host-side
 // outer loop of lpa_run (lpa.py:262-308).
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <vector>
@@ -60,7 +61,8 @@ void upload_csr(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *off, const i
     g.ids.release();
     g.pos.release();
     g.has_order = 0;
-    g.base.release();
+    // buffers are reused when large enough (repeated lpa_run calls re-upload
+    // the graph; freeing and re-allocating GBs would dominate)
     g.base.n = n;
     g.base.m = m;
     g.base.off.alloc(n + 1);
@@ -68,9 +70,11 @@ void upload_csr(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *off, const i
     CUDA_TRY(cudaMemcpyAsync(g.base.off.p, off, (n + 1) * sizeof(int64_t), kind, s));
     if (m) CUDA_TRY(cudaMemcpyAsync(g.base.tgt.p, tgt, m * sizeof(int32_t), kind, s));
     if (w_f64) {
+        g.base.w32.release();
         g.base.w64.alloc(m);
         if (m) CUDA_TRY(cudaMemcpyAsync(g.base.w64.p, w, m * sizeof(double), kind, s));
     } else {
+        g.base.w64.release();
         g.base.w32.alloc(m);
         if (m) CUDA_TRY(cudaMemcpyAsync(g.base.w32.p, w, m * sizeof(float), kind, s));
     }
@@ -221,12 +225,21 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     ctx->g.bin_hi.release();
     ctx->g.bin_giant.release();
     ctx->g.giant_off.release();
+    ctx->g.sort_k1.release();
+    ctx->g.sort_k2.release();
+    ctx->g.sort_small.release();
+    ctx->g.sort_v.release();
     WorkBuffers &wb = ctx->wb;
     wb.lab_old.release(); wb.lab_new.release(); wb.flag_a.release(); wb.flag_b.release();
     wb.dirty_a.release(); wb.dirty_b.release(); wb.wl_lo.release(); wb.wl_mid.release(); wb.wl_hi.release(); wb.wl_giant.release();
     wb.glab.release(); wb.gw.release();
     wb.io_labels.release(); wb.io_flags.release(); wb.counters.release(); wb.metric_d.release();
     wb.metric_u.release(); wb.scratch.release();
+    wb.hparts.release(); wb.hmeta.release(); wb.dirty_g.release(); wb.dirty_gp.release();
+    wb.dirty_bytes.release(); wb.dcount.release();
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_n = 0;
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -345,9 +358,12 @@ int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int
         require_graph(ctx);
         SLPA_REQUIRE(delta_history && iterations && converged, SLPA_EINVAL, "output pointers are NULL");
         DeviceGraph &g = ctx->g;
+        const auto tp0 = std::chrono::steady_clock::now();
         slpa_ensure_bins(ctx, cfg);
         check_gpu_limits(ctx, cfg);
         slpa_alloc_work(ctx);
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        const auto tp1 = std::chrono::steady_clock::now();
         reset_stats(ctx);
         ctx->have_labels = 0;
         const bool det = cfg->worker_count == 0;
@@ -383,7 +399,14 @@ int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int
         *iterations = it;
         *converged = conv;
         ctx->have_labels = 1;
+        const auto tp2 = std::chrono::steady_clock::now();
         if (labels_out) slpa_labels_to_host(ctx, labels_out);
+        if (getenv("SLPA_TRACE")) {
+            const auto tp3 = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            fprintf(stderr, "[slpa] run phases: bins+alloc %.2f ms, sweeps %.2f ms (device %.2f), labels D2H %.2f ms\n",
+                    ms(tp0, tp1), ms(tp1, tp2), (double)ctx->stats.device_ms, ms(tp2, tp3));
+        }
     });
 }
 

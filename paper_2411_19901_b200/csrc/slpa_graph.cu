@@ -428,6 +428,100 @@ void slpa_check_int_weights(slpa_ctx *ctx) {
     bad.release();
 }
 
+// ------------------------------------------------------------------ fused arc checks
+// One arc-parallel pass: a block takes kArcBlock consecutive arcs, thread 0
+// finds the rows they span, every thread locates the row of its first arc by
+// a binary search inside that span and walks its kArcPer arcs.  Per arc: the
+// symmetry multiset hashes of (u, t) and (t, u) (two independent 32-bit
+// mixes summed in 64 bits), and the integral-weight test with the maximum
+// weight; per row start: the maximum degree.  Replaces a warp-per-row pass
+// whose hub rows serialised on one warp.
+constexpr int kArcBlock = 2048, kArcPer = 8;
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x85ebca6bu;
+    x ^= x >> 13;
+    x *= 0xc2b2ae35u;
+    x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ int64_t row_of(const int64_t *off, int64_t lo, int64_t hi, int64_t e) {
+    while (lo < hi) {  // largest r in [lo, hi] with off[r] <= e
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(&off[mid]) <= e) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <class W>
+__global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const int32_t *tgt, const W *w, int64_t n,
+                                                    int64_t m, unsigned long long *acc, unsigned *bad,
+                                                    unsigned long long *wmax, unsigned long long *dmax) {
+    __shared__ int64_t s_r[2];
+    const int64_t e0 = (int64_t)blockIdx.x * kArcBlock;
+    if (e0 >= m) return;
+    const int64_t e1 = min(m, e0 + kArcBlock);
+    if (threadIdx.x == 0) {
+        s_r[0] = row_of(off, 0, n - 1, e0);
+        s_r[1] = row_of(off, s_r[0], n - 1, e1 - 1);
+    }
+    __syncthreads();
+    unsigned long long f1 = 0, r1 = 0, f2 = 0, r2 = 0, mw = 0, md = 0;
+    bool ok = true;
+    const int64_t a0 = e0 + (int64_t)threadIdx.x * kArcPer;
+    if (a0 < e1) {
+        int64_t u = row_of(off, s_r[0], s_r[1], a0);
+        int64_t start = __ldg(&off[u]), next = __ldg(&off[u + 1]);
+        uint32_t hu1 = fmix32((uint32_t)u ^ 0x9e3779b9u), hu2 = fmix32((uint32_t)u ^ 0x7f4a7c15u);
+        if (start >= a0) md = (unsigned long long)(next - start);
+        for (int j = 0; j < kArcPer; ++j) {
+            const int64_t e = a0 + j;
+            if (e >= e1) break;
+            while (e >= next) {
+                ++u;
+                start = next;
+                next = __ldg(&off[u + 1]);
+                hu1 = fmix32((uint32_t)u ^ 0x9e3779b9u);
+                hu2 = fmix32((uint32_t)u ^ 0x7f4a7c15u);
+                const unsigned long long d = (unsigned long long)(next - start);
+                md = d > md ? d : md;
+            }
+            const uint32_t t = (uint32_t)__ldg(&tgt[e]);
+            const uint32_t ht1 = fmix32(t ^ 0x9e3779b9u), ht2 = fmix32(t ^ 0x7f4a7c15u);
+            f1 += fmix32(hu1 + t);
+            r1 += fmix32(ht1 + (uint32_t)u);
+            f2 += fmix32(hu2 ^ (t * 0x2545f491u));
+            r2 += fmix32(ht2 ^ ((uint32_t)u * 0x2545f491u));
+            const double x = (double)__ldg(&w[e]);
+            ok &= (x >= 1.0) && (x == floor(x)) && (x < 2147483648.0);
+            const unsigned long long xi = ok ? (unsigned long long)x : 0ull;
+            mw = xi > mw ? xi : mw;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+        f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        const unsigned long long ow = __shfl_xor_sync(0xffffffffu, mw, o), od = __shfl_xor_sync(0xffffffffu, md, o);
+        mw = ow > mw ? ow : mw;
+        md = od > md ? od : md;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&acc[0], f1);
+        atomicAdd(&acc[1], r1);
+        atomicAdd(&acc[2], f2);
+        atomicAdd(&acc[3], r2);
+        atomicMax(wmax, mw);
+        atomicMax(dmax, md);
+        if (!ok) atomicOr(bad, 1u);
+    }
+}
+
 // Symmetry check + reverse CSR of the active numbering; resets the bins.
 void slpa_graph_finalize(slpa_ctx *ctx) {
     DeviceGraph &g = ctx->g;
@@ -438,18 +532,30 @@ void slpa_graph_finalize(slpa_ctx *ctx) {
     g.roff.release();
     g.rsrc.release();
     g.symmetric = 1;
-    slpa_check_int_weights(ctx);
+    g.int_weights = 1;
     if (g.n == 0 || g.m == 0) return;
+    // acc: 4 hashes, bad flag, max weight, max degree (one readback)
     DevBuf<unsigned long long> acc;
-    acc.alloc(4);
-    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 4 * sizeof(unsigned long long), s));
-    k_sym_hash<<<grid_warps(g.n), kT, 0, s>>>(g.off(), g.tgt(), g.n, acc.p);
+    acc.alloc(8);
+    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 8 * sizeof(unsigned long long), s));
+    const unsigned blocks = (unsigned)((g.m + kArcBlock - 1) / kArcBlock);
+    if (g.w_f64)
+        k_arc_checks<double><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const double *)g.w(), g.n, g.m, acc.p,
+                                                      (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
+    else
+        k_arc_checks<float><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const float *)g.w(), g.n, g.m, acc.p,
+                                                     (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
     CUDA_TRY(cudaGetLastError());
-    unsigned long long h[4];
+    unsigned long long h[8];
     CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     acc.release();
     g.symmetric = (h[0] == h[1]) && (h[2] == h[3]);
+    // integer sketch values need integral weights and every weighted degree
+    // < 2^31: max weight x max degree < 2^31 settles it; otherwise the exact
+    // per-row sums decide
+    if ((unsigned)h[4] != 0u) g.int_weights = 0;
+    else if ((double)h[5] * (double)h[6] >= 2147483648.0) slpa_check_int_weights(ctx);
     if (g.symmetric) return;
     // reverse CSR: in-degree histogram, exclusive scan, atomic fill
     g.roff.alloc(g.n + 1);
@@ -584,8 +690,8 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
     if (n > 0)
         k_classify<<<grid_for(n, kT), kT, 0, s>>>(g.off(), n, cfg->degree_threshold, hsplit, gsplit, single, g.cls.p);
     CUDA_TRY(cudaGetLastError());
-    DevBuf<int64_t> cnt;
-    cnt.alloc(4);
+    DevBuf<int64_t> &cnt = g.sort_small;  // persistent scratch: bins are rebuilt on every upload
+    cnt.alloc(8);
     cub::CountingInputIterator<int32_t> it(0);
     const uint8_t classes[4] = {CLS_LO, CLS_MID, CLS_HI, CLS_GIANT};
     int32_t *outs[4] = {g.bin_lo.p, g.bin_mid.p, g.bin_hi.p, g.bin_giant.p};
@@ -611,8 +717,8 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
                                         : (which == 1 ? g.n_mid : (lo_sorted ? g.n_lo : 0));
         int32_t *binp = outs[which];
         if (cntb <= 1) continue;
-        DevBuf<int64_t> dk, dk2;
-        DevBuf<int32_t> v2;
+        DevBuf<int64_t> &dk = g.sort_k1, &dk2 = g.sort_k2;
+        DevBuf<int32_t> &v2 = g.sort_v;
         dk.alloc(cntb);
         dk2.alloc(cntb);
         v2.alloc(cntb);
@@ -620,23 +726,27 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
         int64_t *k1 = dk.p, *k2 = dk2.p;
         int32_t *v1 = binp, *vv2 = v2.p;
         const int64_t nh = cntb;
+        // degree keys: low / mid bins are bounded by their split, so few radix passes
+        const int64_t kmax = (which == 0 && !single) ? (int64_t)cfg->degree_threshold
+                                                     : (which == 1 ? (int64_t)hsplit : (1LL << 40));
+        int end_bit = 1;
+        while (end_bit < 40 && (1LL << end_bit) <= kmax) ++end_bit;
         if (which >= 2)
             cub_call(ctx, [&](void *tmp, size_t &bytes) {
-                return cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k1, k2, v1, vv2, nh, 0, 40, s);
+                return cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k1, k2, v1, vv2, nh, 0, end_bit, s);
             });
         else
             cub_call(ctx, [&](void *tmp, size_t &bytes) {
-                return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, v1, vv2, nh, 0, 40, s);
+                return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, v1, vv2, nh, 0, end_bit, s);
             });
         CUDA_TRY(cudaMemcpyAsync(binp, v2.p, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
     }
     // giant gather-buffer offsets: exclusive prefix of the giants' degrees
     g.giant_off.alloc(g.n_giant + 1);
     g.giant_arcs = 0;
     g.giant_max_deg = 0;
     if (g.n_giant > 0) {
-        DevBuf<int64_t> dk;
+        DevBuf<int64_t> &dk = g.sort_k1;
         dk.alloc(g.n_giant + 1);
         CUDA_TRY(cudaMemsetAsync(dk.p, 0, (g.n_giant + 1) * sizeof(int64_t), s));
         k_bin_degrees<<<grid_for(g.n_giant, kT), kT, 0, s>>>(g.off(), g.bin_giant.p, g.n_giant, dk.p);
@@ -648,8 +758,8 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
         CUDA_TRY(cudaMemcpyAsync(first2, g.giant_off.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         g.giant_max_deg = first2[1] - first2[0];
-        dk.release();
     }
+    CUDA_TRY(cudaStreamSynchronize(s));
     g.bin_thr = cfg->degree_threshold;
     g.bin_single = single;
     g.bin_lo_sorted = lo_sorted;

@@ -130,6 +130,8 @@ struct DeviceGraph {
     DevBuf<uint8_t> cls;
     DevBuf<int32_t> bin_lo, bin_mid, bin_hi, bin_giant;
     DevBuf<int64_t> giant_off;  // exclusive prefix of giant degrees (n_giant + 1)
+    DevBuf<int64_t> sort_k1, sort_k2, sort_small;  // binning scratch, kept across uploads
+    DevBuf<int32_t> sort_v;
     int64_t n_lo = 0, n_mid = 0, n_hi = 0, n_giant = 0, giant_arcs = 0, giant_max_deg = 0;
     const Csr &act() const { return has_order ? perm : base; }
     const int64_t *off() const { return act().off.p; }
@@ -175,6 +177,8 @@ struct slpa_ctx {
     DeviceGraph g;
     WorkBuffers wb;
     unsigned long long *h_counters = nullptr;  // pinned mirror of wb.counters (striped)
+    int32_t *h_stage = nullptr;                // pinned staging for label downloads
+    int64_t h_stage_n = 0;
     unsigned long long h_sum[CNT_N] = {};      // per-counter sums of the stripes
     std::string err;
     slpa_run_stats stats{};

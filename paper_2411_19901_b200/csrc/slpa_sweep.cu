@@ -21,6 +21,8 @@
 // Async mode (worker_count > 0) is the paper's in-place parallel sweep.
 #include <algorithm>
 #include <chrono>
+#include <cstring>
+#include <thread>
 #include <vector>
 #include <cstdlib>
 #include "slpa_eval.cuh"
@@ -1020,8 +1022,28 @@ void slpa_labels_to_host(slpa_ctx *ctx, int32_t *host) {
         CUDA_TRY(cudaGetLastError());
         src = ctx->wb.io_labels.p;
     }
-    CUDA_TRY(cudaMemcpyAsync(host, src, n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    // through a pinned staging buffer (full-speed DMA), then a parallel host copy
+    if (ctx->h_stage_n < n) {
+        if (ctx->h_stage) CUDA_TRY(cudaFreeHost(ctx->h_stage));
+        ctx->h_stage = nullptr;
+        CUDA_TRY(cudaMallocHost((void **)&ctx->h_stage, (size_t)n * sizeof(int32_t)));
+        ctx->h_stage_n = n;
+    }
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_stage, src, n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const int nt = n >= (1 << 22) ? 8 : 1;
+    if (nt == 1) {
+        std::memcpy(host, ctx->h_stage, (size_t)n * sizeof(int32_t));
+    } else {
+        std::vector<std::thread> th;
+        const int64_t per = (n + nt - 1) / nt;
+        for (int i = 0; i < nt; ++i) {
+            const int64_t b = i * per, e = std::min<int64_t>(n, b + per);
+            if (b < e)
+                th.emplace_back([=] { std::memcpy(host + b, ctx->h_stage + b, (size_t)(e - b) * sizeof(int32_t)); });
+        }
+        for (auto &t : th) t.join();
+    }
 }
 
 void slpa_labels_from_host(slpa_ctx *ctx, const int32_t *host) {
