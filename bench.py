@@ -177,6 +177,13 @@ def run_reference_arm(args, world, rank):
 
 
 def workload_config(args, n, m, world):
+    if getattr(args, "graph", "rmat") != "rmat":
+        name = {"grid": "4899x4899 4-neighbour grid, unit weights, permuted ids (configs[2])",
+                "kmer": "k-mer-like chain graph, 2e8 vertices, links kept w.p. 0.95 + n/20 chords, permuted ids (configs[3])"}
+        return {"workload": f"nu{'MG8' if args.variant == 'mg' else 'BM'}-LPA {args.graph} ({name[args.graph]})",
+                "graph": name[args.graph], "vertices": n, "arcs": m, "variant": args.variant,
+                "mode": "deterministic (bit-exact sequential)" if args.mode == "det" else "async",
+                "parallelism": "single GPU", "l2_policy": "inputs larger than L2"}
     return {
         "workload": f"nuMG8-LPA RMAT s{args.scale} ef16 (configs[1])" if args.variant == "mg"
         else f"nuBM-LPA RMAT s{args.scale} ef16",
@@ -259,6 +266,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--graph", default="rmat", choices=["rmat", "grid", "kmer"],
+                    help="rmat: configs[1] (default); grid: configs[2] 4899^2 grid; kmer: configs[3] 2e8-vertex k-mer-like")
     ap.add_argument("--variant", default="mg", choices=["mg", "bm"])
     ap.add_argument("--mode", default="det", choices=["det", "async"])
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -284,7 +293,12 @@ def main():
         run_partitioned(args, world, rank, local, dist)
         return
     eng = slpa.Engine(local)
-    eng.gen_rmat(args.scale, seed=SEED, permute=True)
+    if args.graph == "grid":
+        eng.gen_grid(4899, 4899, permute=True)
+    elif args.graph == "kmer":
+        eng.gen_kmer(200_000_000, seed=3)
+    else:
+        eng.gen_rmat(args.scale, seed=SEED, permute=True)
     n, m = eng.n, eng.m
     cfg = slpa.LpaConfig(variant=args.variant, worker_count=0 if args.mode == "det" else 1)
 
@@ -336,7 +350,8 @@ def main():
     if os.path.exists(tfile):  # written by tools/ncu_traffic.py from an ncu capture of the same workload
         with open(tfile) as f:
             tj = json.load(f)
-        if tj.get("scale") == args.scale and tj.get("variant") == args.variant and tj.get("mode") == args.mode:
+        if (tj.get("scale") == args.scale and tj.get("variant") == args.variant and tj.get("mode") == args.mode
+                and tj.get("graph", "rmat") == args.graph):
             c = tj.get("classes", {}).get(dom_name)
             traffic = c.get("dram_bytes_per_launch") if c else None
 

@@ -61,6 +61,16 @@ int64_t lo_small_max() {
     return m;
 }
 
+// Round 0 of a deterministic sweep launches the light vertices from a
+// flag-compacted copy of their bin (1, default) or over the whole bin (0).
+int round0_compact() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_R0_COMPACT");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
 // Giants run asynchronously across rounds (1, default) or are joined every
 // round (0).
 int giant_async_mode() {
@@ -596,6 +606,38 @@ __global__ void k_move_class(const int32_t *__restrict__ bin, int64_t count, uin
     if (atomicAnd(&from[v >> 5], ~bit) & bit) atomicOr(&to[v >> 5], bit);
 }
 
+// Round-0 worklist of a later sweep: the flagged entries of a degree-ordered
+// bin, order kept within a block (one atomic per block).
+__global__ void __launch_bounds__(kThreads) k_filter_flags(const int32_t *__restrict__ bin, int64_t count,
+                                                           const uint8_t *__restrict__ flags,
+                                                           int32_t *__restrict__ out,
+                                                           unsigned long long *__restrict__ cursor) {
+    __shared__ int s_warp[kThreads / 32];
+    __shared__ unsigned long long s_base;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t v = 0;
+    bool hit = false;
+    if (i < count) {
+        v = __ldg(&bin[i]);
+        hit = flags[v] != 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s_warp[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int j = 0; j < kThreads / 32; ++j) {
+            const int c = s_warp[j];
+            s_warp[j] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(cursor, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    if (hit) out[s_base + s_warp[w] + __popc(m & ((1u << lane) - 1))] = v;
+}
+
 // Multi-GPU deterministic sweep: dirty marks cross ranks as bytes (NCCL has
 // no bitwise-OR reduction; a MAX over 0/1 bytes is the OR).
 __global__ void k_dirty_bits_to_bytes(const uint32_t *__restrict__ bits, uint8_t *__restrict__ bytes, int64_t n) {
@@ -765,7 +807,24 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
         launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
     }
-    launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    // Round 0, light vertices: only the flagged entries of the degree-ordered
+    // bin.  After sweep 0 a minority is flagged; launching the whole bin would
+    // leave most lanes of every warp idle while the few flagged ones run the
+    // full evaluation.
+    if (g.n_lo > 0 && round0_compact()) {
+        unsigned long long *c0 = wb.counters.p + CNT_LO * CNT_STRIPES;
+        timed_launch(ctx, SLPA_PROF_COMPACT, 1, [&] {
+            k_filter_flags<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(g.bin_lo.p, g.n_lo, wb.flag_a.p,
+                                                                          wb.wl_lo.p, c0);
+            CUDA_TRY(cudaGetLastError());
+        });
+        unsigned long long nf = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nf, c0, sizeof(nf), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, (int64_t)nf, 1, SLPA_PROF_EVAL_LO0);
+    } else {
+        launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    }
     int64_t rounds = 1;
     unsigned long long evals0 = 0, arcs0 = 0;
     bool first = true;

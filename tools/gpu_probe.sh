@@ -1,3 +1,8 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-SLPA_TRACE=1 timeout 600 python tools/e2e_prof.py --scale 24 --reps 4 2>&1 | grep -v "sweep round\|L2 pers" > gpurun_out/e2e.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_paths.py tests/test_gpu_parity.py tests/test_gpu_configs.py -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+run() { echo "=== $*"; env "$@" timeout 300 python tools/prof_run.py $G --runs 4 | tail -1; }
+{
+G="--scale 24"; run SLPA_X=0; run SLPA_R0_COMPACT=0
+G="--graph grid --scale 24"; run SLPA_X=0; run SLPA_R0_COMPACT=0
+G="--graph kmer --scale 27"; run SLPA_X=0; run SLPA_R0_COMPACT=0
+} > gpurun_out/ab.log 2>&1
