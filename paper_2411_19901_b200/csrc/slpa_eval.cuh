@@ -747,8 +747,17 @@ __global__ void __launch_bounds__(kThreads, SLPA_LO_MINB) k_lane_direct(SweepArg
     Pol pol;
     pol.init(a.k, cur, deg, a.parts);
     bool lower_changed = false;
-    lane_stream<W, DET>(a, lo, deg, v, lower_changed,
-                        [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
+    // Rows of a warp have similar lengths (degree-ordered bins).  Short rows
+    // stream unaligned -- element j of every lane is arc j of its own row, so
+    // a warp of degree-d rows runs d accumulate steps; aligned 32-byte
+    // batches would scatter those arcs over all 8 batch slots.
+    const unsigned maxdeg = __reduce_max_sync(0xffffffffu, (unsigned)deg);
+    if (maxdeg <= 8)
+        lane_stream_u<W, DET>(a, lo, deg, v, lower_changed,
+                              [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
+    else
+        lane_stream<W, DET>(a, lo, deg, v, lower_changed,
+                            [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
     if (go && deg) pol.finish();
     if (Pol::kHasRescan && a.scan_double) {
         pol.rescan_begin();
