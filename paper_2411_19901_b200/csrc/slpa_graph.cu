@@ -741,6 +741,17 @@ void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
             });
         CUDA_TRY(cudaMemcpyAsync(binp, v2.p, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
+    // largest light degree (the low bin is degree-ascending when sorted)
+    g.lo_max_deg = single ? INT64_MAX : (int64_t)cfg->degree_threshold - 1;
+    if (g.n_lo > 0 && lo_sorted && !single) {
+        int32_t vlast = 0;
+        CUDA_TRY(cudaMemcpyAsync(&vlast, g.bin_lo.p + g.n_lo - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        int64_t o2[2] = {0, 0};
+        CUDA_TRY(cudaMemcpyAsync(o2, g.off() + vlast, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        g.lo_max_deg = o2[1] - o2[0];
+    }
     // giant gather-buffer offsets: exclusive prefix of the giants' degrees
     g.giant_off.alloc(g.n_giant + 1);
     g.giant_arcs = 0;

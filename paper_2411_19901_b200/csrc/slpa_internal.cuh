@@ -133,6 +133,7 @@ struct DeviceGraph {
     DevBuf<int64_t> sort_k1, sort_k2, sort_small;  // binning scratch, kept across uploads
     DevBuf<int32_t> sort_v;
     int64_t n_lo = 0, n_mid = 0, n_hi = 0, n_giant = 0, giant_arcs = 0, giant_max_deg = 0;
+    int64_t lo_max_deg = 0;  // largest degree in the low bin
     const Csr &act() const { return has_order ? perm : base; }
     const int64_t *off() const { return act().off.p; }
     const int32_t *tgt() const { return act().tgt.p; }

@@ -31,7 +31,7 @@ namespace {
 
 // Next-round worklists from one pass over the dirty bitmap (1, default) or
 // from passes over every degree bin (0); rounds with more light vertices
-// than kScanSortMin re-derive the degree-ordered list from the bins.
+// than scan_sort_min() re-derive the degree-ordered list from the bins.
 int scan_mode() {
     static const int m = [] {
         const char *e = getenv("SLPA_SCAN");
@@ -39,7 +39,13 @@ int scan_mode() {
     }();
     return m;
 }
-constexpr int64_t kScanSortMin = 32768;
+int64_t scan_sort_min() {
+    static const int64_t m = [] {
+        const char *e = getenv("SLPA_SCAN_SORT_MIN");
+        return e ? atoll(e) : 32768LL;
+    }();
+    return m;
+}
 
 // High-degree rounds with at most this many vertices use the block-per-vertex
 // slot-parallel scan (short chains) instead of the warp-per-vertex one.
@@ -57,6 +63,15 @@ int64_t lo_small_max() {
     static const int64_t m = [] {
         const char *e = getenv("SLPA_LO_SMALL");
         return e ? atoll(e) : 2048LL;
+    }();
+    return m;
+}
+
+// Light-vertex commit in position order (1, default) or over the bin (0).
+int commit_pos_mode() {
+    static const int m = [] {
+        const char *e = getenv("SLPA_COMMIT_POS");
+        return e ? atoi(e) : 1;
     }();
     return m;
 }
@@ -638,6 +653,32 @@ __global__ void __launch_bounds__(kThreads) k_filter_flags(const int32_t *__rest
     if (hit) out[s_base + s_warp[w] + __popc(m & ((1u << lane) - 1))] = v;
 }
 
+// Commit of the light vertices in position order (coalesced label words):
+// a changed light vertex folds L1 into L0 and marks its neighbours t <= v.
+__global__ void __launch_bounds__(kThreads) k_commit_lo_pos(SweepArgs a, int64_t n) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long d = 0;
+    if (v < n) {
+        const uint32_t wv = a.lab_new[v];
+        if ((wv & SLPA_CHG) && a.cls[v] == CLS_LO) {
+            const int32_t c = (int32_t)(wv & SLPA_LMASK);
+            a.lab_old[v] = c;
+            a.lab_new[v] = (uint32_t)c;
+            d = 1;
+            const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+            for (int64_t e0 = lo; e0 < hi; e0 += 8) {
+                int32_t t[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) t[j] = e0 + j < hi ? __ldg(&a.tgt[e0 + j]) : INT32_MAX;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (t[j] <= v) a.flag_next[t[j]] = 1;
+            }
+        }
+    }
+    warp_count(a.counters, 0, 0, d);
+}
+
 // Multi-GPU deterministic sweep: dirty marks cross ranks as bytes (NCCL has
 // no bitwise-OR reduction; a MAX over 0/1 bytes is the OR).
 __global__ void k_dirty_bits_to_bytes(const uint32_t *__restrict__ bits, uint8_t *__restrict__ bytes, int64_t n) {
@@ -892,7 +933,8 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             CUDA_TRY(cudaGetLastError());
         });
         read_counters(ctx);
-        if (bitmap_scan && (int64_t)ctx->h_sum[CNT_LO] > kScanSortMin) {
+        // (rows of at most 8 arcs stream unaligned, so their order matters little)
+        if (bitmap_scan && (int64_t)ctx->h_sum[CNT_LO] > scan_sort_min() && g.lo_max_deg > 8) {
             // large round: the degree-ordered worklist keeps the lanes of a warp on similar row lengths
             CUDA_TRY(cudaMemsetAsync(cur_lo, 0, sizeof(unsigned long long), s));
             timed_launch(ctx, SLPA_PROF_COMPACT, 1, [&] {
@@ -995,7 +1037,10 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             CUDA_TRY(cudaGetLastError());
         });
     } else timed_launch(ctx, SLPA_PROF_COMMIT, 4, [&] {
-        if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
+        if (g.n_lo > 0) {
+            if (commit_pos_mode()) k_commit_lo_pos<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, n);
+            else k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
+        }
         if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
         if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
         if (g.n_giant > 0)

@@ -67,6 +67,7 @@ ENVS = [
     {"SLPA_HI_SMALL": "100000000"},
     {"SLPA_LO_SMALL": "0"},
     {"SLPA_R0_COMPACT": "0", "SLPA_GIANT": "300"},
+    {"SLPA_COMMIT_POS": "0", "SLPA_SCAN_SORT_MIN": "0"},
     {"SLPA_LO_SMALL": "100000000", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "1000", "SLPA_HI_SPLIT": "300"},
     {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
