@@ -310,8 +310,8 @@ __device__ __forceinline__ void ld8(const int32_t *p, int32_t (&r)[8], uint64_t 
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "l"(p), "l"(pol));
 }
-__device__ __forceinline__ void ld8(const uint32_t *p, uint32_t (&r)[8]) {
-    asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+__device__ __forceinline__ void ld8(const uint32_t *p, uint32_t (&r)[8]) {  // scratch read once: streaming
+    asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "l"(p));
 }
@@ -329,13 +329,13 @@ __device__ __forceinline__ void ld8(const double *p, double (&r)[8], uint64_t po
                  : "l"(p + 4), "l"(pol));
 }
 __device__ __forceinline__ void ld8_cg(const float *p, float (&r)[8]) {
-    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
                  : "l"(p));
 }
 __device__ __forceinline__ void ld8_cg(const double *p, double (&r)[8]) {
-    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
-    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[4]), "=d"(r[5]), "=d"(r[6]), "=d"(r[7]) : "l"(p + 4));
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[4]), "=d"(r[5]), "=d"(r[6]), "=d"(r[7]) : "l"(p + 4));
 }
 
 // Unaligned flavour for short ranges (the chunks of a high-degree row): the
@@ -1034,10 +1034,12 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
     uint32_t *dst = a.hparts + (size_t)wid * kLpmWords;
     uint4 *kd = reinterpret_cast<uint4 *>(dst + lane * 8);
     uint4 *vd = reinterpret_cast<uint4 *>(dst + 256 + lane * 8);
-    kd[0] = make_uint4((uint32_t)part.key[0], (uint32_t)part.key[1], (uint32_t)part.key[2], (uint32_t)part.key[3]);
-    kd[1] = make_uint4((uint32_t)part.key[4], (uint32_t)part.key[5], (uint32_t)part.key[6], (uint32_t)part.key[7]);
-    vd[0] = make_uint4((uint32_t)part.val[0], (uint32_t)part.val[1], (uint32_t)part.val[2], (uint32_t)part.val[3]);
-    vd[1] = make_uint4((uint32_t)part.val[4], (uint32_t)part.val[5], (uint32_t)part.val[6], (uint32_t)part.val[7]);
+    // streaming stores: the scratch is read once by the merge and must not
+    // push the label array out of L2
+    __stcs(kd, make_uint4((uint32_t)part.key[0], (uint32_t)part.key[1], (uint32_t)part.key[2], (uint32_t)part.key[3]));
+    __stcs(kd + 1, make_uint4((uint32_t)part.key[4], (uint32_t)part.key[5], (uint32_t)part.key[6], (uint32_t)part.key[7]));
+    __stcs(vd, make_uint4((uint32_t)part.val[0], (uint32_t)part.val[1], (uint32_t)part.val[2], (uint32_t)part.val[3]));
+    __stcs(vd + 1, make_uint4((uint32_t)part.val[4], (uint32_t)part.val[5], (uint32_t)part.val[6], (uint32_t)part.val[7]));
     if (lane == 0) a.hmeta[wid] = make_uint2((uint32_t)cur, 1u | (f0 ? 2u : 0u) | (lca ? 4u : 0u));
 }
 
@@ -1501,8 +1503,8 @@ __global__ void __launch_bounds__(kGatherThreads) k_giant_gather(SweepArgs a, co
         if (DET && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
         const int64_t e = e0 + j;
         if (e < hi) {
-            a.glab[base + e] = L[j];
-            gw[base + e] = t[j] == v ? (W)0 : w[j];
+            __stcs(&a.glab[base + e], L[j]);  // read once by the replay: keep L2 for the labels
+            __stcs(&gw[base + e], t[j] == v ? (W)0 : w[j]);
         }
     }
 }
