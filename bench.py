@@ -108,6 +108,8 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SLPA_BENCH_SHARE_GPU"):  # test harness: every rank on GPU 0 (gloo)
+        local = 0
     return world, rank, local
 
 
@@ -286,7 +288,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # NCCL between GPUs; SLPA_BENCH_BACKEND=gloo lets tests run the same
+        # path with several ranks on one device
+        dist.init_process_group(os.environ.get("SLPA_BENCH_BACKEND", "nccl"))
 
     import paper_2411_19901_b200 as slpa
     if world > 1:

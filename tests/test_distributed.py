@@ -326,3 +326,23 @@ def test_gpu_deterministic_partition_bit_exact(oracle, variant, world):
         assert hist == ref.delta_history
         assert (iters, conv) == (ref.iterations, ref.converged)
         np.testing.assert_array_equal(lab, ref.labels)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["det", "async"])
+def test_bench_multi_rank_path(mode):
+    """bench.py's N > 1 path end to end under torchrun: two ranks share one
+    B200 over gloo (the driver's scaling run uses NCCL on N GPUs)."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SLPA_BENCH_BACKEND="gloo", SLPA_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(repo, "bench.py"), "--gpus", "2", "--scale",
+           "15", "--steps", "2", "--warmup", "1", "--mode", mode]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=repo)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["vertices"] == 1 << 16
