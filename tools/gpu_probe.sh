@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-run() { echo "=== $*"; env "$@" timeout 300 python tools/prof_run.py $G --runs 6 | tail -2; }
-{
-G="--scale 24"; run SLPA_X=0; run SLPA_GIANT=65536; run SLPA_GIANT=131072; run SLPA_GIANT=262144; run SLPA_X=0
-} > gpurun_out/ab.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_final.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_final.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_final.log 2>&1
