@@ -137,6 +137,13 @@ int32_t slpa_gen_kmer(slpa_ctx *ctx, int64_t n, uint32_t keep, uint64_t seed, in
 int32_t slpa_build_graph(slpa_ctx *ctx, int64_t n, int64_t num_edges, const int64_t *src,
                          const int64_t *dst, const double *w, int32_t weights_f64);
 
+/* validate_graph (graph.py:378-403) on the resident graph, checks in the
+ * reference's order: code 1 = vertex `*vertex` has a neighbour list that is
+ * not strictly increasing, 2 = non-positive weight, 3 = arc set not
+ * symmetric (incl. reverse weights), 0 = passed; deg_sum / total are the two
+ * sides of the degree-sum identity the caller tests with math.isclose. */
+int32_t slpa_validate_graph(slpa_ctx *ctx, int32_t *code, int64_t *vertex, double *deg_sum, double *total);
+
 /* ------------------------------------------------------------ label propagation
  * lpa_run (lpa.py:262-308).  labels_out: host int32[n] or NULL (labels stay
  * resident, fetch with slpa_get_labels).  delta_history: host int64[max_iterations]. */
@@ -200,6 +207,64 @@ int32_t slpa_part_det_commit(slpa_ctx *ctx, const slpa_config *cfg, int64_t *cha
  * reduced incident array and the summed internal weight. */
 int32_t slpa_part_tally(slpa_ctx *ctx, double *internal_local, uint64_t *incident_dptr, uint64_t *sizes_dptr);
 int32_t slpa_part_modularity(slpa_ctx *ctx, double internal_total, double *q);
+
+
+/* ------------------------------------------------------------ graph files
+ * Parallel host parsers / writers for load_graph / write_edgelist /
+ * write_matrix_market (graph.py:165-375).  slpa_edges_parse reads a file into
+ * (src, dst, w) entries with the reference's per-line rules and error order
+ * (graph.py:165-197 edge lists incl. _remap_ids :200-218; :221-288
+ * MatrixMarket, 0-based); the entries then go to slpa_build_graph for the
+ * device assembly.  Status codes below; err_line is the 1-based line the
+ * reference's message names.  SLPA_IO_EXOTIC: the file needs Python's own
+ * text decoding / integer rules (non-ASCII bytes, digit underscores, ids
+ * beyond 18 digits) -- the caller parses it itself. */
+enum { SLPA_FORMAT_EDGE_LIST = 0, SLPA_FORMAT_MATRIX_MARKET = 1 };
+enum {
+    SLPA_IO_OK = 0,
+    SLPA_IO_EL_FIELDS = 101,      /* "expected 'src dst [weight]', got {aux} fields"  graph.py:173-176 */
+    SLPA_IO_EL_NONINT = 102,      /* "non-integer vertex id"                          :177-181 */
+    SLPA_IO_EL_NEGATIVE = 103,    /* "negative vertex id"                             :182-183 */
+    SLPA_IO_EL_BADWEIGHT = 104,   /* "malformed weight"                               :185-188 */
+    SLPA_IO_EL_WEIGHT = 105,      /* "weight must be positive and finite"             :189-190 */
+    SLPA_IO_NO_EDGES = 106,       /* "{path}: no edges found"                         :195-196, :285-286 */
+    SLPA_IO_MM_HEADER = 110,      /* "not a MatrixMarket matrix file"                 :222-225 */
+    SLPA_IO_MM_LAYOUT = 111,      /* :227-228 */
+    SLPA_IO_MM_FIELD = 112,       /* :229-230 */
+    SLPA_IO_MM_SYMMETRY = 113,    /* :231-232 */
+    SLPA_IO_MM_NOSIZE = 114,      /* :242-243 */
+    SLPA_IO_MM_SIZE_FIELDS = 115, /* :245-246 */
+    SLPA_IO_MM_SIZE_NONINT = 116, /* :247-250 */
+    SLPA_IO_MM_NOT_SQUARE = 117,  /* aux x aux2                                       :251-252 */
+    SLPA_IO_MM_EMPTY = 118,       /* :253-254 */
+    SLPA_IO_MM_ENTRY_FIELDS = 119,/* aux = fields wanted                              :262-263 */
+    SLPA_IO_MM_NONINT = 120,      /* :264-268 */
+    SLPA_IO_MM_RANGE = 121,       /* :269-270 */
+    SLPA_IO_MM_BADVALUE = 122,    /* :272-275 */
+    SLPA_IO_MM_VALUE = 123,       /* :276-277 */
+    SLPA_IO_MM_COUNT = 124,       /* declared aux, found aux2                         :283-284 */
+    SLPA_IO_EXOTIC = 190,
+    SLPA_IO_OSERROR = 191,
+    SLPA_IO_NOMEM = 192
+};
+typedef struct slpa_edges slpa_edges;
+/* threads <= 0: all hardware threads.  *out is set (free it) whenever the
+ * return value is not SLPA_IO_OSERROR. */
+int32_t slpa_edges_parse(const char *path, int32_t format, int32_t threads, slpa_edges **out);
+int32_t slpa_edges_info(const slpa_edges *e, int64_t *count, int64_t *n, int32_t *remapped, int32_t *err,
+                        int64_t *err_line, int64_t *err_aux, int64_t *err_aux2);
+/* raw_ids: int64[n] dense id -> id in the file (edge lists with remapped ids). */
+int32_t slpa_edges_copy(const slpa_edges *e, int64_t *src, int64_t *dst, double *w, int64_t *raw_ids);
+void slpa_edges_free(slpa_edges *e);
+/* Canonical writers (graph.py:352-375): text of rows [row_begin, row_end),
+ * one "i j w" line per arc with i <= j (lower = 0, edge list) or
+ * "i+1 j+1 w" per arc with i >= j (lower = 1, MatrixMarket body), weights as
+ * "%.6g".  *buf is malloc'ed (free with slpa_free_buffer). */
+int64_t slpa_format_count(int64_t n, const int64_t *offsets, const int32_t *targets, int32_t lower);
+int32_t slpa_format_rows(int64_t row_begin, int64_t row_end, const int64_t *offsets, const int32_t *targets,
+                         const void *weights, int32_t weights_f64, int32_t lower, int32_t threads, char **buf,
+                         int64_t *len);
+void slpa_free_buffer(char *buf);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@ libslpa_b200.so (hand-written sm_100a CUDA) through a C ABI
 
 from .engine import Engine, default_engine, keep_threshold, rmat_thresholds
 from .graph import Graph, GraphLoadError, build_graph, build_graph_arrays
+from .graph_io import load_graph, validate_graph, write_edgelist, write_matrix_market
 from .lpa import LpaConfig, LpaResult, aux_memory_estimate, lpa_move, lpa_run
 from .metrics import CommunityStats, community_stats, modularity
 
@@ -28,8 +29,12 @@ __all__ = [
     "community_stats",
     "default_engine",
     "keep_threshold",
+    "load_graph",
     "lpa_move",
     "lpa_run",
     "modularity",
     "rmat_thresholds",
+    "validate_graph",
+    "write_edgelist",
+    "write_matrix_market",
 ]

@@ -108,6 +108,18 @@ SIGNATURES = {
     "slpa_part_det_commit": (_i32, [_vp, ctypes.POINTER(SlpaConfig), ctypes.POINTER(_i64)]),
     "slpa_part_tally": (_i32, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "slpa_part_modularity": (_i32, [_vp, _d, ctypes.POINTER(_d)]),
+    "slpa_validate_graph": (_i32, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_d),
+                                   ctypes.POINTER(_d)]),
+    "slpa_edges_parse": (_i32, [ctypes.c_char_p, _i32, _i32, ctypes.POINTER(_vp)]),
+    "slpa_edges_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32),
+                               ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                               ctypes.POINTER(_i64)]),
+    "slpa_edges_copy": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "slpa_edges_free": (None, [_vp]),
+    "slpa_format_count": (_i64, [_i64, _vp, _vp, _i32]),
+    "slpa_format_rows": (_i32, [_i64, _i64, _vp, _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(ctypes.c_void_p),
+                                ctypes.POINTER(_i64)]),
+    "slpa_free_buffer": (None, [_vp]),
 }
 
 _LIB = None

@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
           defines: list[str] | None = None) -> str:
     """Build the library (incremental).  `out` / `defines` build an A/B variant
     (timing experiments only) into a separate object directory."""
-    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     lib = out or LIB
     obj_dir = OBJ if not out else os.path.join(os.path.dirname(os.path.abspath(out)), "_obj_" + os.path.basename(out))
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _deps_mtime():
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     extra += ["-D" + d for d in (defines or [])]
 
     def compile_one(src):
-        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.splitext(os.path.basename(src))[0] + ".o")
         cmd = [nvcc] + NVCC_FLAGS + extra + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

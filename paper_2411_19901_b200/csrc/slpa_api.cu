@@ -14,6 +14,7 @@ void slpa_gen_grid_impl(slpa_ctx *ctx, int64_t rows, int64_t cols, int32_t permu
 void slpa_gen_kmer_impl(slpa_ctx *ctx, int64_t n, uint32_t keep, uint64_t seed, int32_t permute, uint64_t perm_key);
 void slpa_build_graph_impl(slpa_ctx *ctx, int64_t n, int64_t ne, const int64_t *src, const int64_t *dst,
                            const double *w, int32_t weights_f64);
+void slpa_validate_graph_impl(slpa_ctx *ctx, int32_t *code, int64_t *vertex, double *deg_sum, double *total);
 
 namespace {
 thread_local std::string g_create_err;
@@ -348,6 +349,13 @@ int32_t slpa_build_graph(slpa_ctx *ctx, int64_t n, int64_t num_edges, const int6
         slpa_build_graph_impl(ctx, n, num_edges, src, dst, w, weights_f64);
         slpa_graph_finalize(ctx);
         ctx->have_labels = 0;
+    });
+}
+
+int32_t slpa_validate_graph(slpa_ctx *ctx, int32_t *code, int64_t *vertex, double *deg_sum, double *total) {
+    return guard(ctx, [&] {
+        require_graph(ctx);
+        slpa_validate_graph_impl(ctx, code, vertex, deg_sum, total);
     });
 }
 

@@ -119,6 +119,14 @@ class Engine:
                                                                w.ctypes.data))
         return off, tgt[: self.m], w[: self.m]
 
+    def validate(self):
+        """validate_graph on the resident graph: (code, vertex, deg_sum, total)."""
+        code, vertex = ctypes.c_int32(), ctypes.c_int64()
+        ds, tot = ctypes.c_double(), ctypes.c_double()
+        check(self.lib, self.ctx, self.lib.slpa_validate_graph(self.ctx, ctypes.byref(code), ctypes.byref(vertex),
+                                                               ctypes.byref(ds), ctypes.byref(tot)))
+        return code.value, vertex.value, ds.value, tot.value
+
     def gen_rmat(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, permute=True, perm_key=7):
         ta, tab, tabc = rmat_thresholds(a, b, c)
         rc = self.lib.slpa_gen_rmat(self.ctx, int(scale), int(edge_factor) << int(scale), ta, tab, tabc,
