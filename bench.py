@@ -14,12 +14,21 @@ convergence) from fresh labels.
 * e2e    : same metric through the public API ``lpa_run(graph, cfg)`` with
            the graph in pinned HOST memory: H2D upload + validation + binning
            + run + D2H labels inside the timed region.
-* roofline: dominant kernel class from the engine's profiling mode (CUDA
+* roofline: dominant kernel family from the engine's profiling mode (CUDA
            events around each launch on its stream): algorithmic bytes
            (18 B per evaluated vertex + 12 B per scanned arc) /
-           device time, against MEASURED_PEAKS.json hbm_gbs.
-* cpu_baseline: the CPU oracle (C restatement of the reference) on this
-           host, 1 thread, a bounded prefix of sweep 0 on the same graph.
+           device time, against MEASURED_PEAKS.json hbm_gbs; `traffic` from
+           an ncu capture of one run (profiles/ncu_traffic.json) on the same
+           launch basis; `run_frac` = the whole run's algorithmic bytes
+           (first evaluations only) over its device time.
+* parity / quality: the GPU result checked against a complete sequential
+           lpa_run of the oracle port on the same graph (labels, delta
+           history, iterations), modularity and community count of both.
+* cpu_baseline: that oracle run's time (1 thread; the algorithm is
+           sequential), plus the Python reference itself (baseline/_ref):
+           a full C1 run and a bounded sweep-0 prefix of the bench graph.
+* --impl reference: complete oracle-port lpa_run's of the same workload on
+           the host (time-budgeted, --ref-budget), the same unit of work.
 * N > 1  : one RMAT graph of scale --scale + log2(N) partitioned by contiguous
            vertex ranges; deterministic mode (default): speculative rounds
            across ranks, NCCL all-gather of the owned label words + MAX-reduce
@@ -36,6 +45,7 @@ import statistics
 import subprocess
 import sys
 import time
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -47,6 +57,12 @@ UNIT = "arcs*iters/s"
 SEED = 2411
 ALG_BYTES_PER_VERTEX = 18
 ALG_BYTES_PER_ARC = 12
+# kernel families for the roofline (engine profiling classes they sum)
+FAMILIES = {
+    "eval_hi": ("eval_hi_r0", "eval_hi_rk", "eval_mid_r0", "eval_mid_rk"),  # deg >= D_H (k_mg_hi_*, k_bm_hi_*)
+    "eval_lo": ("eval_lo_r0", "eval_lo_rk"),                                # deg < D_H (k_lane_direct, k_lo_warp)
+    "eval_giant": ("eval_giant",),                                          # deg >= 32768 (gather + block replay)
+}
 
 
 def peaks():
@@ -113,67 +129,122 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_baseline_sample(host_graph, variant, seconds):
-    """The oracle's sequential sweep 0 over a growing vertex prefix for about
-    `seconds` of CPU time; returns (arcs/s, sample description)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_full_runs(host_graph, cfg, budget_s, max_runs):
+    """Complete sequential lpa_run's of the CPU oracle (oracle/lpa_oracle.c,
+    the C restatement of lpa.py:262-308, pinned to the reference's golden
+    vectors) on the bench graph, 1 host thread, until `budget_s` is spent
+    (at least one run).  Returns (runs, result of the last run)."""
     from oracle.oracle import get_oracle
-    import paper_2411_19901_b200 as slpa
     orc = get_oracle()
-    cfg = slpa.LpaConfig(variant=variant)
-    n = host_graph.num_vertices
+    runs, res, spent = [], None, 0.0
+    while len(runs) < max(1, max_runs) and (not runs or spent + runs[-1][0] <= budget_s):
+        t0 = time.perf_counter()
+        res = orc.lpa_run(host_graph, cfg)
+        dt = time.perf_counter() - t0
+        spent += dt
+        runs.append((dt, res.iterations))
+    return runs, res
+
+
+def python_reference_sample(host_graph, variant, seconds):
+    """The Python reference itself (baseline/_ref: sketchlpa 0.1.0, pip-
+    installed by tools/install_reference.sh) on the host, BASELINE.md §2:
+    a complete lpa_run on C1 (tests/golden c1) and -- C2 takes ~50 min in
+    Python -- sweep 0 of the bench graph over a vertex prefix of about
+    `seconds` through the reference's own sweep (lpa._process_vertices,
+    lpa.py:204-224).  perf_counter around the call as cli.py:182-184."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "sketchlpa")):
+        return {"unavailable": "baseline/_ref not installed (tools/install_reference.sh)"}
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import sketchlpa
+    from sketchlpa import lpa as ref_lpa
+    out = {"impl": "sketchlpa 0.1.0 (Python, pure numpy/loops)", "cores": 1}
+    gold = os.path.join(REPO, "tests", "golden", "golden_sbm.npz")
+    if os.path.exists(gold):
+        z = np.load(gold)
+        g1 = sketchlpa.Graph(z["c1/offsets"], z["c1/targets"], z["c1/weights"])
+        t0 = time.perf_counter()
+        r1 = sketchlpa.lpa_run(g1, sketchlpa.LpaConfig(variant=variant))
+        dt = time.perf_counter() - t0
+        out["c1_full_run"] = {"seconds": dt, "iterations": r1.iterations,
+                              "value": g1.num_arcs * r1.iterations / dt, "unit": UNIT,
+                              "modularity": float(sketchlpa.modularity(g1, r1.labels)),
+                              "num_communities": int(sketchlpa.community_stats(g1, r1.labels).num_communities)}
+    g = sketchlpa.Graph(host_graph.offsets, host_graph.targets, host_graph.weights)
+    cfg = sketchlpa.LpaConfig(variant=variant)
+    n = g.num_vertices
     labels = np.arange(n, dtype=np.int32)
-    flags = np.ones(n, dtype=np.uint8)
-    off = host_graph.offsets
-    pos, arcs, t_total = 0, 0, 0.0
-    chunk = 4096
-    while t_total < seconds and pos < n:
+    unprocessed = np.ones(n, dtype=bool)
+    sel = ref_lpa._make_selector(g, labels, cfg)
+    pos, arcs, spent, chunk = 0, 0, 0.0, 2048
+    while spent < seconds and pos < n:
         hi = min(n, pos + chunk)
         t0 = time.perf_counter()
-        orc.lpa_move_range(host_graph, labels, flags, cfg, True, pos, hi)
-        t_total += time.perf_counter() - t0
-        arcs += int(off[hi] - off[pos])
+        ref_lpa._process_vertices(g, labels, unprocessed, sel, True, range(pos, hi))
+        spent += time.perf_counter() - t0
+        arcs += int(g.offsets[hi] - g.offsets[pos])
         pos = hi
-        chunk = min(chunk * 2, 1 << 20)
-    return arcs / t_total, f"sweep 0 (pick-less) over vertices [0, {pos}) of {n}: {arcs} arcs in {t_total:.1f} s"
+        chunk = min(chunk * 2, 65536)
+    out["bench_graph_sweep0_prefix"] = {"vertices": pos, "arcs": arcs, "seconds": spent, "value": arcs / spent,
+                                        "unit": "arcs/s (sweep 0, pick-less; every vertex active)"}
+    return out
 
 
 def run_reference_arm(args, world, rank):
-    """--impl reference: the CPU oracle (restatement of the reference's
-    sequential LPA), 1 host thread, bounded samples of the same workload."""
+    """--impl reference: the reference's CPU implementation of the path on
+    this host.  The reference is Python and cannot be compiled, so per the
+    tier rules the arm is the oracle port (oracle/lpa_oracle.c, the C
+    restatement, pinned to the reference's golden vectors): COMPLETE
+    lpa_run's of the same graph and config as the GPU arm -- the same unit
+    of work, |E| x iterations / wall -- 1 host thread (the deterministic
+    algorithm is sequential).  Steps are time-budgeted (--ref-budget); the
+    line says how many ran.  The Python reference itself is timed beside it
+    (python_reference)."""
     if rank != 0:
         return
-    from oracle.oracle import get_oracle
     import paper_2411_19901_b200 as slpa
+    from oracle.oracle import get_oracle
     orc = get_oracle()
     t0 = time.perf_counter()
-    g = orc.rmat(args.scale, seed=SEED, permute=True)
+    if args.graph == "grid":
+        g = orc.grid(4899, 4899, permute=True)
+    elif args.graph == "kmer":
+        g = orc.kmer(200_000_000, seed=3)
+    else:
+        g = orc.rmat(args.scale, seed=SEED, permute=True)
     gen_s = time.perf_counter() - t0
     cfg = slpa.LpaConfig(variant=args.variant)
-    n = g.num_vertices
-    vals = []
-    samples = []
-    for step in range(args.warmup + args.steps):
-        labels = np.arange(n, dtype=np.int32)
-        flags = np.ones(n, dtype=np.uint8)
-        lo = (step * 131071) % max(n - 200000, 1)
-        hi = min(n, lo + args.ref_prefix)
-        t0 = time.perf_counter()
-        orc.lpa_move_range(g, labels, flags, cfg, True, lo, hi)
-        dt = time.perf_counter() - t0
-        arcs = int(g.offsets[hi] - g.offsets[lo])
-        if step >= args.warmup:
-            vals.append(arcs / dt)
-            samples.append((lo, hi, arcs, dt))
-    value = float(np.median(vals))
-    sample = (f"sweep-0 vertex ranges of {args.ref_prefix} vertices (first [{samples[0][0]},{samples[0][1]})), "
-              f"RMAT s{args.scale} ef16, {g.num_arcs} arcs; graph generated on CPU in {gen_s:.0f} s")
+    runs, res = oracle_full_runs(g, cfg, args.ref_budget, args.steps)
+    secs = [r[0] for r in runs]
+    value = g.num_arcs * sum(r[1] for r in runs) / sum(secs)
+    sample = (f"{len(runs)} complete sequential lpa_run(s) (oracle port, deterministic, {res.iterations} "
+              f"iterations each) on {args.graph} n={g.num_vertices} m={g.num_arcs}; "
+              f"graph generated on the CPU in {gen_s:.0f} s (outside the timing)")
+    pyref = python_reference_sample(g, args.variant, args.py_seconds) if args.py_seconds > 0 else None
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean([s[3] for s in samples])),
+        "steps": len(runs), "steps_requested": args.steps, "warmup": 0, "warmup_requested": args.warmup,
+        "ms_per_step": 1000.0 * float(np.mean(secs)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args, g.num_vertices, g.num_arcs, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
+                         "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "python_reference": pyref},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result": {"iterations": res.iterations, "delta_history": res.delta_history,
+                   "num_communities": int(np.unique(res.labels).size)},
     }
     print(json.dumps(line), flush=True)
 
@@ -273,8 +344,10 @@ def main():
     ap.add_argument("--variant", default="mg", choices=["mg", "bm"])
     ap.add_argument("--mode", default="det", choices=["det", "async"])
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-prefix", type=int, default=400000)
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="reference arm: CPU seconds of complete oracle runs (at least one run)")
+    ap.add_argument("--py-seconds", type=float, default=10.0,
+                    help="Python reference sample (baseline/_ref) beside the CPU numbers; 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
@@ -317,6 +390,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     t_dev, iters_all, launches = 0.0, [], 0
+    stats_sum = {"first_evals": 0, "first_arcs": 0, "vertex_evals": 0, "arc_reads": 0, "rounds": 0}
     wall0 = time.perf_counter()
     for _ in range(args.steps):
         _, iters, delta, conv = eng.run(cfg, fetch_labels=False)
@@ -324,6 +398,8 @@ def main():
         t_dev += st["device_ms"]
         iters_all.append(iters)
         launches += st["kernel_launches"]
+        for k in stats_sum:
+            stats_sum[k] += st[k]
     barrier()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
@@ -344,26 +420,40 @@ def main():
     eng.run(cfg, fetch_labels=False)
     prof = eng.profile()
     eng.set_profiling(False)
-    dom_name, dom = max(((k, v) for k, v in prof.items() if k.startswith("eval")), key=lambda kv: kv[1]["ms"])
+    fams = {}
+    for fam, members in FAMILIES.items():
+        fams[fam] = {k: sum(prof[c][k] for c in members) for k in ("launches", "ms", "evals", "arcs")}
+    dom_name, dom = max(fams.items(), key=lambda kv: kv[1]["ms"])
     alg_bytes = ALG_BYTES_PER_VERTEX * dom["evals"] + ALG_BYTES_PER_ARC * dom["arcs"]
     achieved = alg_bytes / (dom["ms"] / 1000.0) / 1e9 if dom["ms"] > 0 else 0.0
     peak, peak_src = peaks()
     total_ms = sum(v["ms"] for v in prof.values())
-    traffic = None
+    traffic, traffic_run = None, None
     tfile = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):  # written by tools/ncu_traffic.py from an ncu capture of the same workload
+    if os.path.exists(tfile):  # tools/ncu_traffic.py over an ncu capture of ONE lpa_run of this workload
         with open(tfile) as f:
             tj = json.load(f)
         if (tj.get("scale") == args.scale and tj.get("variant") == args.variant and tj.get("mode") == args.mode
-                and tj.get("graph", "rmat") == args.graph):
-            c = tj.get("classes", {}).get(dom_name)
-            traffic = c.get("dram_bytes_per_launch") if c else None
+                and tj.get("graph", "rmat") == args.graph and tj.get("basis") == "one lpa_run"):
+            c = tj.get("families", {}).get(dom_name)
+            if c and dom["launches"]:
+                traffic_run = c["dram_bytes_per_run"]
+                traffic = traffic_run / dom["launches"]  # same launch count as alg_bytes_per_launch
+    # run level: bytes of the vertices each sweep processes
+    # (first evaluation only: re-evaluations are overhead) over the whole run
+    run_alg = (ALG_BYTES_PER_VERTEX * stats_sum["first_evals"] + ALG_BYTES_PER_ARC * stats_sum["first_arcs"]) \
+        / args.steps
+    run_achieved = run_alg / (t_s / args.steps) / 1e9
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     host_graph = None
+    int_path = False
     if rank == 0 or world > 1:
         off, tgt, w = eng.download()
+        # the device's exactness test for integer sketch values (slpa_graph.cu)
+        wdeg = np.add.reduceat(w.astype(np.float64), off[:-1]) if w.size else np.zeros(1)
+        int_path = bool(np.all(w == np.floor(w)) and (wdeg[np.diff(off) > 0].max(initial=0) < 2.0 ** 31))
         pin_off = torch.empty(off.size, dtype=torch.int64, pin_memory=True).numpy()
         pin_tgt = torch.empty(tgt.size, dtype=torch.int32, pin_memory=True).numpy()
         pin_w = torch.empty(w.size, dtype=torch.float32, pin_memory=True).numpy()
@@ -396,17 +486,47 @@ def main():
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": e2e_steps, "s_per_step": e2e_t / e2e_steps}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and host_graph is not None:
-        v, sample = cpu_baseline_sample(host_graph, args.variant, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
-               "host_cpus": os.cpu_count()}
+    cpu, parity, quality = None, None, None
+    if rank == 0 and world == 1 and host_graph is not None:
+        # the GPU result of this workload, checked against the reference's
+        # sequential algorithm (oracle port) on the same graph: labels,
+        # delta history, iterations; quality (Q, |communities|) beside it
+        labels_gpu, it_gpu, delta_gpu, conv_gpu = eng.run(cfg)
+        q_gpu, nc_gpu = eng.tally(labels_gpu, want_arrays=False)[:2]
+        quality = {"gpu": {"modularity": q_gpu, "num_communities": int(nc_gpu), "iterations": it_gpu,
+                           "delta_history": delta_gpu}}
+        if not args.no_cpu_baseline:
+            from oracle.oracle import get_oracle
+            runs, ref = oracle_full_runs(host_graph, slpa.LpaConfig(variant=args.variant), 0.0, 1)
+            q_ref = get_oracle().modularity(host_graph, ref.labels)
+            nc_ref = int(np.unique(ref.labels).size)
+            quality["cpu_reference"] = {"modularity": q_ref, "num_communities": nc_ref,
+                                        "iterations": ref.iterations, "delta_history": ref.delta_history}
+            if args.mode == "det":
+                parity = {"vs": "oracle port: complete sequential lpa_run on the same graph",
+                          "labels_equal": bool(np.array_equal(labels_gpu, ref.labels)),
+                          "delta_history_equal": delta_gpu == ref.delta_history,
+                          "iterations_equal": it_gpu == ref.iterations, "converged_equal": conv_gpu == ref.converged}
+            else:
+                parity = {"vs": "sequential oracle (async acceptance: |dQ| <= 0.01, communities within 5%)",
+                          "dQ": q_gpu - q_ref, "communities_ratio": nc_gpu / max(1, nc_ref)}
+            cpu = {"value": float(m) * ref.iterations / runs[0][0], "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"one complete sequential lpa_run (oracle port, {ref.iterations} iterations) on the "
+                             f"bench graph: {runs[0][0]:.1f} s",
+                   "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
+            if args.py_seconds > 0:
+                cpu["python_reference"] = python_reference_sample(host_graph, args.variant, args.py_seconds)
 
     if rank == 0:
+        dev_b, graph_b = stats_last["device_bytes"], stats_last["graph_bytes"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * t_s / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32" if int_path else "f64",
+            "dtype_note": ("u32: sketch / vote values in uint32, exact (bit-identical to the reference's "
+                           "binary64) because every weight is integral and every weighted degree < 2^31, checked "
+                           "on the device at upload; otherwise the binary64 kernels run"),
+            "data": "synthetic",
             "config": workload_config(args, n, m, world),
             "iterations_per_step": iters_all,
             "wall_s_timed": wall,
@@ -416,13 +536,27 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom_name,
                          "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes / max(dom["launches"], 1),
+                         "launches_per_run": dom["launches"],
+                         "alg_bytes_per_run": alg_bytes, "traffic_per_run": traffic_run,
                          "ms_per_launch": dom["ms"] / max(dom["launches"], 1),
                          "share_of_step": dom["ms"] / total_ms if total_ms else None,
-                         "profile": prof},
+                         "run_alg_bytes": run_alg, "run_achieved": run_achieved, "run_frac": run_achieved / peak,
+                         "basis": ("per launch: the family's algorithmic bytes (18 B per evaluated vertex + 12 B "
+                                   "per scanned arc, re-evaluations included) and its ncu DRAM bytes over ONE "
+                                   "lpa_run, both divided by the same kernel-launch count; run_frac: 18 B per "
+                                   "processed vertex + 12 B per arc of it, first evaluations only, over the "
+                                   "whole run's device time"),
+                         "families": fams, "profile": prof},
+            "memory": {"device_bytes": dev_b, "graph_bytes": graph_b,
+                       "device_bytes_per_vertex": dev_b / max(n, 1), "device_bytes_per_arc": dev_b / max(m, 1),
+                       "engine_bytes_per_vertex": (dev_b - graph_b) / max(n, 1),
+                       "reference_model_aux_bytes": slpa.aux_memory_estimate(
+                           SimpleNamespace(num_vertices=n, weights=np.zeros(0, eng.weights_dtype)), cfg)},
+            "quality": quality,
+            "parity": parity,
             "cpu_baseline": cpu,
             "clocks": clk,
-            "run_stats": {k: stats_last[k] for k in ("rounds", "vertex_evals", "arc_reads", "first_evals",
-                                                     "first_arcs", "device_bytes", "graph_bytes")},
+            "run_stats": {k: v / args.steps for k, v in stats_sum.items()},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -20,6 +20,8 @@ ap.add_argument("--variant", default="mg")
 ap.add_argument("--mode", default="det")
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--range", action="store_true",
+                help="cudaProfilerStart/Stop around the LAST run only (ncu --profile-from-start off)")
 a = ap.parse_args()
 eng = slpa.Engine(0)
 if a.graph == "rmat":
@@ -36,9 +38,20 @@ if off is not None:
           "arcs in hi:", int(deg[deg >= 128].sum()))
 cfg = slpa.LpaConfig(variant=a.variant, worker_count=0 if a.mode == "det" else 1)
 eng.set_profiling(a.profile)
+rt = None
+if a.range:
+    import ctypes
+    rt = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    if rt is None:
+        import torch
+        rt = torch.cuda.cudart()
 for r in range(a.runs):
     t0 = time.perf_counter()
+    if rt is not None and r == a.runs - 1:
+        rt.cudaProfilerStart()
     labels, iters, delta, conv = eng.run(cfg, fetch_labels=False)
+    if rt is not None and r == a.runs - 1:
+        rt.cudaProfilerStop()
     st = eng.stats()
     print(f"run {r}: iters {iters} delta {delta} device_ms {st['device_ms']:.2f} wall {1e3*(time.perf_counter()-t0):.1f}")
 if a.profile:
