@@ -452,8 +452,9 @@ def main():
     if rank == 0 or world > 1:
         off, tgt, w = eng.download()
         # the device's exactness test for integer sketch values (slpa_graph.cu)
-        wdeg = np.add.reduceat(w.astype(np.float64), off[:-1]) if w.size else np.zeros(1)
-        int_path = bool(np.all(w == np.floor(w)) and (wdeg[np.diff(off) > 0].max(initial=0) < 2.0 ** 31))
+        nz = np.diff(off) > 0  # reduceat needs in-range starts: non-empty rows only
+        wdeg = np.add.reduceat(w.astype(np.float64), off[:-1][nz]) if w.size else np.zeros(0)
+        int_path = bool(np.all(w == np.floor(w)) and (wdeg.max(initial=0) < 2.0 ** 31))
         pin_off = torch.empty(off.size, dtype=torch.int64, pin_memory=True).numpy()
         pin_tgt = torch.empty(tgt.size, dtype=torch.int32, pin_memory=True).numpy()
         pin_w = torch.empty(w.size, dtype=torch.float32, pin_memory=True).numpy()

@@ -135,19 +135,28 @@ void slpa_alloc_work(slpa_ctx *ctx) {
 // Keep the label array the sweeps gather from (lab_new, 4 B per vertex) in
 // L2: an access-policy window on both streams marks it persisting, so the
 // streamed CSR (loaded evict-first) does not push it out.  SLPA_L2_PERSIST_MB
-// caps the set-aside (0 disables).
+// caps the set-aside (default: the device maximum, 79 MiB on the B200, which
+// covers the 64 MiB label words of RMAT s24; 0 disables).  The process-wide
+// limit in force before the first window is saved and restored, and the
+// persisting lines are reset, at the end of every run and in slpa_destroy
+// (release_label_l2_window) so other work in the process gets its L2 back.
 void set_label_l2_window(slpa_ctx *ctx) {
     static const long cap_mb = [] {
         const char *e = getenv("SLPA_L2_PERSIST_MB");
-        return e ? atol(e) : 60L;
+        return e ? atol(e) : 4096L;
     }();
     if (cap_mb <= 0 || ctx->g.n == 0) return;
     int max_persist = 0, max_window = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
     CUDA_TRY(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
     const size_t want = (size_t)ctx->g.n * sizeof(uint32_t);
-    const size_t setaside = std::min<size_t>((size_t)max_persist, (size_t)cap_mb << 20);
+    const size_t setaside = std::min<size_t>(std::min<size_t>((size_t)max_persist, (size_t)cap_mb << 20),
+                                             (want + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1));
     if (setaside == 0 || max_window <= 0) return;
+    if (!ctx->l2_saved) {
+        CUDA_TRY(cudaDeviceGetLimit(&ctx->l2_prev_limit, cudaLimitPersistingL2CacheSize));
+        ctx->l2_saved = 1;
+    }
     CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
     cudaStreamAttrValue attr{};
     attr.accessPolicyWindow.base_ptr = ctx->wb.lab_new.p;
@@ -160,6 +169,19 @@ void set_label_l2_window(slpa_ctx *ctx) {
     if (getenv("SLPA_TRACE"))
         fprintf(stderr, "[slpa] L2 persisting window: %zu bytes of %zu, set-aside %zu (max %d, window max %d)\n",
                 (size_t)attr.accessPolicyWindow.num_bytes, want, setaside, max_persist, max_window);
+}
+
+// Undo set_label_l2_window: clear the stream windows, demote the persisting
+// lines to normal and restore the process's previous set-aside.
+void release_label_l2_window(slpa_ctx *ctx) {
+    if (!ctx->l2_saved) return;
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.num_bytes = 0;
+    if (ctx->stream) cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+    if (ctx->stream2) cudaStreamSetAttribute(ctx->stream2, cudaStreamAttributeAccessPolicyWindow, &attr);
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->l2_prev_limit);
+    ctx->l2_saved = 0;
 }
 
 static void reset_stats(slpa_ctx *ctx) {
@@ -188,6 +210,7 @@ int32_t slpa_create(int32_t device, slpa_ctx **out) {
                      std::string("libslpa_b200 is built for sm_100a (B200); device is ") + prop.name);
         slpa_ctx *c = new slpa_ctx();
         c->device = device;
+        c->num_sms = prop.multiProcessorCount;
         try {
             CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             CUDA_TRY(cudaEventCreate(&c->ev0));
@@ -214,6 +237,7 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     if (!ctx) return SLPA_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    release_label_l2_window(ctx);
     ctx->g.base.release();
     ctx->g.perm.release();
     ctx->g.ids.release();
@@ -407,6 +431,7 @@ int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int
         *iterations = it;
         *converged = conv;
         ctx->have_labels = 1;
+        release_label_l2_window(ctx);
         const auto tp2 = std::chrono::steady_clock::now();
         if (labels_out) slpa_labels_to_host(ctx, labels_out);
         if (getenv("SLPA_TRACE")) {

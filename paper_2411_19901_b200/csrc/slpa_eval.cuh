@@ -37,6 +37,16 @@ __device__ __forceinline__ int32_t det_label(const SweepArgs &a, int32_t t, int3
 
 __device__ __forceinline__ int32_t async_label(const SweepArgs &a, int32_t t) { return __ldcg(&a.lab_old[t]); }
 
+// One gather per arc (streaming kernels): a lower neighbour's word from
+// lab_new (L1 | changed bit, written this sweep -> L2 load), a higher one's
+// L0 straight from lab_old (read-only during the rounds, no changed bit), so
+// no dependent second load; async mode reads the in-place labels.
+template <bool DET>
+__device__ __forceinline__ uint32_t gather_word(const SweepArgs &a, int32_t t, int32_t v) {
+    if (!DET) return (uint32_t)__ldcg(&a.lab_old[t]);
+    return t < v ? __ldcg(&a.lab_new[t]) : (uint32_t)__ldg(&a.lab_old[t]);
+}
+
 // CSR streams (read once per sweep) are loaded with an L2 evict-first policy
 // so they do not push the label array out of L2.
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -359,12 +369,7 @@ __device__ __forceinline__ void lane_stream_u(const SweepArgs &a, int64_t start,
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             L[j] = 0;
-            if (t[j] != v) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
-        }
-        if (DET) {
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j)
-                if (t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
+            if (t[j] != v) L[j] = gather_word<DET>(a, t[j], v);
         }
         const int64_t nx = x0 + kBatch;
         int32_t tn[kBatch];
@@ -413,7 +418,7 @@ __device__ __forceinline__ void gather_batch(const SweepArgs &a, int32_t v, cons
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
         L[j] = 0;
-        if (t[j] != v) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
+        if (t[j] != v) L[j] = gather_word<DET>(a, t[j], v);
     }
 }
 
@@ -431,11 +436,6 @@ __device__ __forceinline__ void lane_stream_p(const SweepArgs &a, int64_t start,
     for (int64_t x0 = 0;;) {
         gather_batch<DET>(a, v, tB, LB);                                // batch i+1 (masked past the end)
         ld_batch_u<W, DET>(a, wts, start, x0 + 2 * kBatch, len, v, tC, wC);  // batch i+2
-        if (DET) {
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j)
-                if (tA[j] > v && (LA[j] >> 31)) LA[j] = (uint32_t)__ldg(&a.lab_old[tA[j]]);
-        }
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             if (x0 + j < len) {
@@ -481,12 +481,7 @@ __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, i
             inr |= (unsigned)in << j;
             ok |= (unsigned)valid << j;
             L[j] = 0;
-            if (valid) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
-        }
-        if (DET) {  // higher neighbour that changed this sweep: its L0
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j)
-                if (((ok >> j) & 1u) && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
+            if (valid) L[j] = gather_word<DET>(a, t[j], v);
         }
         const int64_t nb = b + kBatch;
         int32_t tn[kBatch];
@@ -610,7 +605,8 @@ struct MgLane {
 #pragma unroll
             for (int i = 0; i < KArr<K>::v; ++i) {
                 if (K == 0 && i >= k) break;
-                if (part.val[i] > (V)0) S.acc(part.key[i], part.val[i], k);
+                const V pv = part.value(i);
+                if (pv > (V)0) S.acc(part.key[i], pv, k);
             }
         }
         part.reset(k);
@@ -785,7 +781,7 @@ __device__ __forceinline__ void warp_merge_parts(WarpSketch<V> &S_, const MgSket
         for (int i = 0; i < KArr<K>::v; ++i) {
             if (K == 0 && i >= k) break;
             int32_t kk = __shfl_sync(0xffffffffu, part.key[i], 0);
-            V vv = __shfl_sync(0xffffffffu, part.val[i], 0);
+            V vv = __shfl_sync(0xffffffffu, part.value(i), 0);
             if (lane == i) { S_.key = kk; S_.val = vv; }
         }
         first = 1;
@@ -795,7 +791,7 @@ __device__ __forceinline__ void warp_merge_parts(WarpSketch<V> &S_, const MgSket
 #pragma unroll
     for (int i = 0; i < KArr<K>::v; ++i) {
         if (K == 0 && i >= k) break;
-        if (part.val[i] > (V)0) nz |= 1u << (i & 31);
+        if (part.value(i) > (V)0) nz |= 1u << (i & 31);
     }
     for (int q = first; q < nb; ++q) {
         const unsigned mq = __shfl_sync(0xffffffffu, nz, q);
@@ -805,7 +801,7 @@ __device__ __forceinline__ void warp_merge_parts(WarpSketch<V> &S_, const MgSket
             if (K == 0 && i >= k) break;
             if (!(mq & (1u << (i & 31)))) continue;
             int32_t c = __shfl_sync(0xffffffffu, part.key[i], q);
-            V w = __shfl_sync(0xffffffffu, part.val[i], q);
+            V w = __shfl_sync(0xffffffffu, part.value(i), q);
             S_.acc(lane, k, c, w);
         }
     }
@@ -938,7 +934,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const
         });
         lch[j] = __any_sync(0xffffffffu, lc);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sp[j][lane][i] = make_uint2((uint32_t)part.key[i], (uint32_t)part.val[i]);
+        for (int i = 0; i < 8; ++i) sp[j][lane][i] = make_uint2((uint32_t)part.key[i], (uint32_t)part.value(i));
     }
     __syncwarp();
     // (B) grouped ordered merge; group g = lanes 8g..8g+7 = vertex g, lane = slot
@@ -1038,8 +1034,8 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
     // push the label array out of L2
     __stcs(kd, make_uint4((uint32_t)part.key[0], (uint32_t)part.key[1], (uint32_t)part.key[2], (uint32_t)part.key[3]));
     __stcs(kd + 1, make_uint4((uint32_t)part.key[4], (uint32_t)part.key[5], (uint32_t)part.key[6], (uint32_t)part.key[7]));
-    __stcs(vd, make_uint4((uint32_t)part.val[0], (uint32_t)part.val[1], (uint32_t)part.val[2], (uint32_t)part.val[3]));
-    __stcs(vd + 1, make_uint4((uint32_t)part.val[4], (uint32_t)part.val[5], (uint32_t)part.val[6], (uint32_t)part.val[7]));
+    __stcs(vd, make_uint4((uint32_t)part.value(0), (uint32_t)part.value(1), (uint32_t)part.value(2), (uint32_t)part.value(3)));
+    __stcs(vd + 1, make_uint4((uint32_t)part.value(4), (uint32_t)part.value(5), (uint32_t)part.value(6), (uint32_t)part.value(7)));
     if (lane == 0) a.hmeta[wid] = make_uint2((uint32_t)cur, 1u | (f0 ? 2u : 0u) | (lca ? 4u : 0u));
 }
 
@@ -1052,13 +1048,13 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_merge(SweepArgs a, const int
     if (!(meta.y & 1u)) return;
     const uint32_t *src = a.hparts + (size_t)idx * kLpmWords;
     MgSketchDev<8, V> S;
+    S.reset(8);
     uint32_t kk[8], vv[8], kn[8], vn[8];
     ld8(src, kk);
     ld8(src + 256, vv);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        S.key[i] = (int32_t)kk[i];
-        S.val[i] = (V)vv[i];
+        S.load_slot(i, (int32_t)kk[i], (V)vv[i]);
     }
     ld8(src + 8, kk);
     ld8(src + 256 + 8, vv);
@@ -1868,7 +1864,7 @@ KernelSet pick_kernels(const slpa_config *cfg) {
             ks.hi_threads = kGrpWarps * 32;
             ks.hi_vpw = kGrp;
         } else if (grouped_ok && hi_grp_mode() == 2) {
-            if (DET) {  // async keeps the fused kernel: labels move within the launch
+            if constexpr (DET) {  // async keeps the fused kernel: labels move within the launch
                 ks.hi = k_mg_hi_scan<W, DET, V>;
                 ks.hi_small = k_mg_hi_block<W, DET, V>;
                 ks.hi_merge = k_mg_hi_merge<W, DET, V>;

@@ -47,10 +47,21 @@ struct SlpaError {
 // the end of a row, so a batch may overhang the last arc of the array.
 constexpr size_t kDevPadBytes = 64;
 
+// Move-only owner: a throw between alloc and release (CUDA_TRY, SLPA_REQUIRE)
+// frees the buffer instead of leaking it.
 template <class T>
 struct DevBuf {
     T *p = nullptr;
     size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), count(o.count) { o.p = nullptr; o.count = 0; }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; count = o.count; o.p = nullptr; o.count = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void alloc(size_t c) {
         if (c <= count && p) return;
         release();
@@ -173,6 +184,7 @@ struct WorkBuffers {
 
 struct slpa_ctx {
     int device = 0;
+    int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DeviceGraph g;
@@ -190,6 +202,8 @@ struct slpa_ctx {
     cudaEvent_t gev0 = nullptr, gev1 = nullptr;
     int32_t giant_pending = 0;
     int32_t have_labels = 0;   // lab_old holds labels of a finished run
+    int32_t l2_saved = 0;      // set_label_l2_window changed the process's persisting set-aside
+    size_t l2_prev_limit = 0;  //   ... which was this before
     // multi-GPU partition
     int32_t part = 0;
     int64_t v_begin = 0, v_end = 0;

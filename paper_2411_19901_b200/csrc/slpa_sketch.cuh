@@ -116,6 +116,11 @@ struct MgSketchDev {
         }
     }
 
+    // slot i's value / load a slot (fresh sketch) / canonical form (no-op here)
+    __device__ __forceinline__ V value(int i) const { return val[i]; }
+    __device__ __forceinline__ void load_slot(int i, int32_t kk, V vv) { key[i] = kk; val[i] = vv; }
+    __device__ __forceinline__ void normalize() {}
+
     __device__ __forceinline__ void clear_values(int k) {  // sketch.py:107-111
         if constexpr (K > 0) {
 #pragma unroll
@@ -154,6 +159,129 @@ struct MgSketchDev {
             V v = val[i];
             if (v > (V)0) {
                 int32_t c = key[i];
+                if (!found || v > bw || (v == bw && c < best)) { best = c; bw = v; found = true; }
+            }
+        }
+        out = best;
+        return found;
+    }
+};
+
+// ---------------------------------------------------------------- integer, k = 8
+// The hot sketch: 8 slots with uint32 values (exact under the integer-value
+// precondition above), branch-free, in the reference's own key
+// representation (every key starts at 0, sketch.py:38).
+//
+// Offset form.  The decrement "every slot loses w, clamped at 0"
+// (sketch.py:71-74) touches all slots; here it is one add: slot i stores
+// s[i] and its value is max(s[i] - D, 0), so the decrement is D += w and a
+// slot is empty exactly when s[i] <= D.  A hit on slot i makes its value
+// value + w, i.e. s[i] = max(s[i], D) + w = max(s[i] + w, D + w) (an empty
+// slot with a stale matching key restarts at w, as values[s] += w on 0.0);
+// an insert writes (c, D + w).  Every quantity stays below the vertex's
+// weighted degree (< 2^31), so nothing wraps.
+//
+// First-match.  keys.index(c) (sketch.py:59-65) is the FIRST slot holding
+// c; with keys starting at 0 label 0 may sit in several slots.  The hit
+// chain carries "no earlier slot matched" in a predicate, so exactly the
+// first matching slot is updated; the insert chain does the same for
+// "first slot with value 0" (sketch.py:66-70).  One accumulate is ~60
+// predicated instructions and no branches, so the lanes of a warp never
+// diverge on hit / insert / decrement.
+template <>
+struct MgSketchDev<8, uint32_t> {
+    int32_t key[8];
+    uint32_t s[8];
+    uint32_t D;
+
+    __device__ __forceinline__ void reset(int) {  // MgSketch.__init__ sketch.py:34-39
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { key[i] = 0; s[i] = 0u; }
+        D = 0u;
+    }
+    __device__ __forceinline__ uint32_t value(int i) const { return s[i] > D ? s[i] - D : 0u; }
+    __device__ __forceinline__ void load_slot(int i, int32_t kk, uint32_t vv) { key[i] = kk; s[i] = vv + D; }
+    __device__ __forceinline__ void normalize() {  // D = 0 form (values stored as-is)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = value(i);
+        D = 0u;
+    }
+
+    // accumulate (sketch.py:47-74)
+    __device__ __forceinline__ void acc(int32_t c, uint32_t w, int) {
+        asm("{\n\t"
+            ".reg .pred a, h;\n\t"
+            ".reg .u32 dw, t;\n\t"
+            "add.u32 dw, %16, %18;\n\t"
+            "setp.ne.s32 a|h, %0, %17;\n\t"
+            "@h add.u32 t, %8, %18;\n\t @h max.u32 %8, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %1, %17, a;\n\t"
+            "@h add.u32 t, %9, %18;\n\t @h max.u32 %9, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %2, %17, a;\n\t"
+            "@h add.u32 t, %10, %18;\n\t @h max.u32 %10, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %3, %17, a;\n\t"
+            "@h add.u32 t, %11, %18;\n\t @h max.u32 %11, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %4, %17, a;\n\t"
+            "@h add.u32 t, %12, %18;\n\t @h max.u32 %12, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %5, %17, a;\n\t"
+            "@h add.u32 t, %13, %18;\n\t @h max.u32 %13, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %6, %17, a;\n\t"
+            "@h add.u32 t, %14, %18;\n\t @h max.u32 %14, t, dw;\n\t"
+            "setp.ne.and.s32 a|h, %7, %17, a;\n\t"
+            "@h add.u32 t, %15, %18;\n\t @h max.u32 %15, t, dw;\n\t"
+            // no hit (a): the first empty slot (s <= D) takes (c, D + w)
+            "setp.gt.and.u32 a|h, %8, %16, a;\n\t @h mov.u32 %0, %17;\n\t @h mov.u32 %8, dw;\n\t"
+            "setp.gt.and.u32 a|h, %9, %16, a;\n\t @h mov.u32 %1, %17;\n\t @h mov.u32 %9, dw;\n\t"
+            "setp.gt.and.u32 a|h, %10, %16, a;\n\t @h mov.u32 %2, %17;\n\t @h mov.u32 %10, dw;\n\t"
+            "setp.gt.and.u32 a|h, %11, %16, a;\n\t @h mov.u32 %3, %17;\n\t @h mov.u32 %11, dw;\n\t"
+            "setp.gt.and.u32 a|h, %12, %16, a;\n\t @h mov.u32 %4, %17;\n\t @h mov.u32 %12, dw;\n\t"
+            "setp.gt.and.u32 a|h, %13, %16, a;\n\t @h mov.u32 %5, %17;\n\t @h mov.u32 %13, dw;\n\t"
+            "setp.gt.and.u32 a|h, %14, %16, a;\n\t @h mov.u32 %6, %17;\n\t @h mov.u32 %14, dw;\n\t"
+            "setp.gt.and.u32 a|h, %15, %16, a;\n\t @h mov.u32 %7, %17;\n\t @h mov.u32 %15, dw;\n\t"
+            // no hit, no empty slot: every slot loses w (the offset grows)
+            "@a mov.u32 %16, dw;\n\t"
+            "}"
+            : "+r"(key[0]), "+r"(key[1]), "+r"(key[2]), "+r"(key[3]), "+r"(key[4]), "+r"(key[5]), "+r"(key[6]),
+              "+r"(key[7]), "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "+r"(s[4]), "+r"(s[5]), "+r"(s[6]),
+              "+r"(s[7]), "+r"(D)
+            : "r"(c), "r"(w));
+    }
+
+    __device__ __forceinline__ void clear_values(int) {  // sketch.py:107-111
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = 0u;
+        D = 0u;
+    }
+
+    // rescan_add (sketch.py:113-126): the first slot whose key equals c gains w
+    // (after clear_values D == 0, so max(s + w, D + w) == s + w).
+    __device__ __forceinline__ void rescan_add(int32_t c, uint32_t w, int) {
+        asm("{\n\t"
+            ".reg .pred a, h;\n\t"
+            "setp.ne.s32 a|h, %8, %16;\n\t @h add.u32 %0, %0, %17;\n\t"
+            "setp.ne.and.s32 a|h, %9, %16, a;\n\t @h add.u32 %1, %1, %17;\n\t"
+            "setp.ne.and.s32 a|h, %10, %16, a;\n\t @h add.u32 %2, %2, %17;\n\t"
+            "setp.ne.and.s32 a|h, %11, %16, a;\n\t @h add.u32 %3, %3, %17;\n\t"
+            "setp.ne.and.s32 a|h, %12, %16, a;\n\t @h add.u32 %4, %4, %17;\n\t"
+            "setp.ne.and.s32 a|h, %13, %16, a;\n\t @h add.u32 %5, %5, %17;\n\t"
+            "setp.ne.and.s32 a|h, %14, %16, a;\n\t @h add.u32 %6, %6, %17;\n\t"
+            "setp.ne.and.s32 a|h, %15, %16, a;\n\t @h add.u32 %7, %7, %17;\n\t"
+            "}"
+            : "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "+r"(s[4]), "+r"(s[5]), "+r"(s[6]), "+r"(s[7])
+            : "r"(key[0]), "r"(key[1]), "r"(key[2]), "r"(key[3]), "r"(key[4]), "r"(key[5]), "r"(key[6]),
+              "r"(key[7]), "r"(c), "r"(w));
+    }
+
+    // max_key (sketch.py:93-105): largest value, ties to the smaller key, skip v <= 0.
+    __device__ __forceinline__ bool max_key(int, int32_t &out) const {
+        bool found = false;
+        int32_t best = 0;
+        uint32_t bw = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t v = value(i);
+            if (v > 0u) {
+                const int32_t c = key[i];
                 if (!found || v > bw || (v == bw && c < best)) { best = c; bw = v; found = true; }
             }
         }
