@@ -419,6 +419,7 @@ def main():
     eng.set_profiling(True)
     eng.run(cfg, fetch_labels=False)
     prof = eng.profile()
+    st_prof = eng.stats()  # profiling run: first_evals / first_arcs = the sequential sweeps' processed set
     eng.set_profiling(False)
     fams = {}
     for fam, members in FAMILIES.items():
@@ -441,8 +442,7 @@ def main():
                 traffic = traffic_run / dom["launches"]  # same launch count as alg_bytes_per_launch
     # run level: bytes of the vertices each sweep processes
     # (first evaluation only: re-evaluations are overhead) over the whole run
-    run_alg = (ALG_BYTES_PER_VERTEX * stats_sum["first_evals"] + ALG_BYTES_PER_ARC * stats_sum["first_arcs"]) \
-        / args.steps
+    run_alg = ALG_BYTES_PER_VERTEX * st_prof["first_evals"] + ALG_BYTES_PER_ARC * st_prof["first_arcs"]
     run_achieved = run_alg / (t_s / args.steps) / 1e9
 
     # ---- e2e through the public API with pinned host buffers
@@ -542,11 +542,13 @@ def main():
                          "ms_per_launch": dom["ms"] / max(dom["launches"], 1),
                          "share_of_step": dom["ms"] / total_ms if total_ms else None,
                          "run_alg_bytes": run_alg, "run_achieved": run_achieved, "run_frac": run_achieved / peak,
+                         "run_processed_vertices": st_prof["first_evals"], "run_processed_arcs": st_prof["first_arcs"],
                          "basis": ("per launch: the family's algorithmic bytes (18 B per evaluated vertex + 12 B "
                                    "per scanned arc, re-evaluations included) and its ncu DRAM bytes over ONE "
                                    "lpa_run, both divided by the same kernel-launch count; run_frac: 18 B per "
-                                   "processed vertex + 12 B per arc of it, first evaluations only, over the "
-                                   "whole run's device time"),
+                                   "vertex the sequential sweeps process + 12 B per arc of it (each sweep's "
+                                   "processed set, counted on the device from the turn bits of the final "
+                                   "evaluations), over the whole run's device time"),
                          "families": fams, "profile": prof},
             "memory": {"device_bytes": dev_b, "graph_bytes": graph_b,
                        "device_bytes_per_vertex": dev_b / max(n, 1), "device_bytes_per_arc": dev_b / max(m, 1),

@@ -62,8 +62,9 @@ typedef struct {
     int64_t rounds;             /* speculative rounds (deterministic mode) */
     int64_t vertex_evals;       /* vertex evaluations incl. re-evaluations */
     int64_t arc_reads;          /* adjacency arcs scanned incl. re-evaluations */
-    int64_t first_evals;        /* evaluations in round 0 of each sweep (= processed vertices) */
-    int64_t first_arcs;         /* arcs scanned in round 0 (algorithmic arcs) */
+    int64_t first_evals;        /* vertices the sequential sweep processes (turn taken), summed over sweeps;
+                                   deterministic mode: profiling runs only (0 otherwise) */
+    int64_t first_arcs;         /* arcs of those vertices (the algorithmic arcs) */
     double  device_ms;          /* device time of the last run (CUDA events) */
     int64_t device_bytes;       /* bytes the context holds on the device */
     int64_t graph_bytes;        /* of which the resident CSR */

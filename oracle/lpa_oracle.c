@@ -299,6 +299,12 @@ int32_t orc_select(const orc_graph *g, const int32_t *labels, int64_t i, const o
     return r;
 }
 
+/* Instrumentation for the tests: vertices processed (flag set when reached,
+ * lpa.py:212-214) and their arcs, accumulated since orc_reset_processed. */
+static int64_t g_proc_vertices, g_proc_arcs;
+void orc_reset_processed(void) { g_proc_vertices = g_proc_arcs = 0; }
+void orc_get_processed(int64_t *out) { out[0] = g_proc_vertices; out[1] = g_proc_arcs; }
+
 static int64_t process_vertices(const orc_graph *g, int32_t *labels, uint8_t *unprocessed,
                                 const orc_config *cfg, int pickless, const int64_t *order,
                                 int64_t lo_pos, int64_t hi_pos, scratch_t *sc) {
@@ -308,6 +314,8 @@ static int64_t process_vertices(const orc_graph *g, int32_t *labels, uint8_t *un
         int64_t i = order ? order[p] : p;
         if (!unprocessed[i]) continue;
         unprocessed[i] = 0;
+        ++g_proc_vertices;
+        g_proc_arcs += g->offsets[i + 1] - g->offsets[i];
         int32_t cand = select_any(g, labels, i, cfg, sc);
         if (cand != labels[i] && (!pickless || cand < labels[i])) {
             labels[i] = cand;

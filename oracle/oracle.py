@@ -187,6 +187,8 @@ class Oracle:
         L.orc_lpa_move_range.argtypes = [vp, vp, vp, vp, i32, vp, i64, i64]
         L.orc_lpa_run.restype = i32
         L.orc_lpa_run.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_reset_processed.argtypes = []
+        L.orc_get_processed.argtypes = [vp]
         L.orc_tally.restype = i32
         L.orc_tally.argtypes = [vp, vp, vp, vp, vp]
         L.orc_aux_memory_estimate.restype = i64
@@ -260,6 +262,16 @@ class Oracle:
         it = iters.value
         return OracleResult(labels, it, [int(x) for x in delta[:it]], bool(conv.value),
                             None if hist is None else hist[:it].copy())
+
+    def processed(self, reset=False):
+        """(vertices, arcs) processed by the sweeps since the last reset
+        (lpa.py:212-214: flag set when the vertex is reached)."""
+        if reset:
+            self.lib.orc_reset_processed()
+            return (0, 0)
+        out = np.zeros(2, dtype=np.int64)
+        self.lib.orc_get_processed(out.ctypes.data)
+        return int(out[0]), int(out[1])
 
     def verify_sweep(self, g, L0, F0, L1, F1, cfg, pickless, vertices=None):
         """Check a GPU sweep (L0,F0) -> (L1,F1) vertex by vertex (ascending

@@ -42,16 +42,6 @@ int32_t guard(slpa_ctx *ctx, F &&f) {
 
 void require_graph(slpa_ctx *ctx) { SLPA_REQUIRE(ctx->g.base.off.p != nullptr, SLPA_ENOGRAPH, "no graph uploaded"); }
 
-void check_gpu_limits(const slpa_ctx *ctx, const slpa_config *cfg) {
-    if (cfg->variant == SLPA_VARIANT_MG) {
-        SLPA_REQUIRE(cfg->sketch_slots <= SLPA_KDYN, SLPA_EUNSUPPORTED,
-                     "sketch_slots > 64 is not supported on the GPU path");
-        if (!cfg->shared_sketch && ctx->g.n_hi + ctx->g.n_giant > 0)
-            SLPA_REQUIRE(cfg->sketch_slots <= SLPA_KHI_MAX, SLPA_EUNSUPPORTED,
-                         "sketch_slots > 32 with high-degree vertices is not supported on the GPU path");
-    }
-}
-
 void upload_csr(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *off, const int32_t *tgt, const void *w,
                 int32_t w_f64, cudaMemcpyKind kind) {
     SLPA_REQUIRE(n >= 0 && m >= 0, SLPA_EINVAL, "negative size");
@@ -126,6 +116,7 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.io_labels.alloc(n);
     wb.io_flags.alloc(n);
     wb.counters.alloc(CNT_TOTAL);
+    if (ctx->prof_on) wb.tbits.alloc(n / 32 + 1);
     CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     if (!ctx->h_counters) CUDA_TRY(cudaMallocHost((void **)&ctx->h_counters, CNT_TOTAL * sizeof(unsigned long long)));
@@ -261,7 +252,7 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     wb.io_labels.release(); wb.io_flags.release(); wb.counters.release(); wb.metric_d.release();
     wb.metric_u.release(); wb.scratch.release();
     wb.hparts.release(); wb.hmeta.release(); wb.dirty_g.release(); wb.dirty_gp.release();
-    wb.dirty_bytes.release(); wb.dcount.release();
+    wb.dirty_bytes.release(); wb.dcount.release(); wb.tbits.release(); wb.xscratch.release();
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     ctx->h_stage = nullptr;
     ctx->h_stage_n = 0;
@@ -392,7 +383,6 @@ int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int
         DeviceGraph &g = ctx->g;
         const auto tp0 = std::chrono::steady_clock::now();
         slpa_ensure_bins(ctx, cfg);
-        check_gpu_limits(ctx, cfg);
         slpa_alloc_work(ctx);
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         const auto tp1 = std::chrono::steady_clock::now();
@@ -400,8 +390,17 @@ int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int
         ctx->have_labels = 0;
         const bool det = cfg->worker_count == 0;
         const int64_t n = g.n;
-        std::vector<int32_t> hook_buf;
-        if (hook) hook_buf.resize((size_t)std::max<int64_t>(n, 1));
+        // The hook gets the live labels (lpa.py:271-273): the caller's output
+        // buffer when given; an edit it makes is uploaded before the next sweep.
+        std::vector<int32_t> hook_buf, hook_prev;
+        int32_t *hb = labels_out;
+        if (hook) {
+            if (!hb) {
+                hook_buf.resize((size_t)std::max<int64_t>(n, 1));
+                hb = hook_buf.data();
+            }
+            hook_prev.resize((size_t)std::max<int64_t>(n, 1));
+        }
         CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
         slpa_init_labels(ctx);
         int32_t it = 0, conv = 0;
@@ -412,9 +411,16 @@ int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int
             ctx->stats.sweeps += 1;
             ++it;
             if (hook) {  // lpa.py:297-298
-                slpa_labels_to_host(ctx, hook_buf.data());
-                if (hook(hook_user, it - 1, pickless, hook_buf.data()) != 0)
+                slpa_labels_to_host(ctx, hb);
+                if (n) std::memcpy(hook_prev.data(), hb, (size_t)n * sizeof(int32_t));
+                if (hook(hook_user, it - 1, pickless, hb) != 0)
                     throw SlpaError{SLPA_EHOOK, "iteration hook raised"};
+                if (n && std::memcmp(hook_prev.data(), hb, (size_t)n * sizeof(int32_t)) != 0) {
+                    if (cfg->variant == SLPA_VARIANT_EXACT)
+                        for (int64_t i = 0; i < n; ++i)
+                            SLPA_REQUIRE(hb[i] >= 0, SLPA_EINVAL, "'list' argument must have no negative elements");
+                    slpa_labels_from_host(ctx, hb);  // the edited live array feeds the next sweep
+                }
             }
             const double frac = n ? (double)delta / (double)n : 0.0;  // lpa.py:299
             if (!pickless && frac < cfg->tolerance) {
@@ -450,10 +456,10 @@ int32_t slpa_move(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels, uint8_
         require_graph(ctx);
         SLPA_REQUIRE(labels && unprocessed && changed, SLPA_EINVAL, "NULL argument");
         const int64_t n = ctx->g.n;
-        for (int64_t i = 0; i < n; ++i)
-            SLPA_REQUIRE(labels[i] >= 0, SLPA_EUNSUPPORTED, "negative labels are not supported on the GPU path");
+        if (cfg->variant == SLPA_VARIANT_EXACT)  // np.bincount rejects negative labels (lpa.py:104)
+            for (int64_t i = 0; i < n; ++i)
+                SLPA_REQUIRE(labels[i] >= 0, SLPA_EINVAL, "'list' argument must have no negative elements");
         slpa_ensure_bins(ctx, cfg);
-        check_gpu_limits(ctx, cfg);
         slpa_alloc_work(ctx);
         reset_stats(ctx);
         if (n == 0) {

@@ -128,10 +128,22 @@ __device__ __forceinline__ void warp_count(unsigned long long *ctr, unsigned lon
     }
 }
 
+// Profiling: record whether v's evaluation took its turn (T).  The last
+// evaluation of a sweep is the fixpoint's, so at the end of the sweep the
+// bitmap is exactly the set of vertices the sequential sweep processes
+// (lpa.py:212-216); vertices never evaluated have T = 0.
+__device__ __forceinline__ void record_turn(const SweepArgs &a, int32_t v, bool T) {
+    if (!a.tbits) return;
+    const uint32_t bit = 1u << (v & 31);
+    if (T) atomicOr(&a.tbits[v >> 5], bit);
+    else atomicAnd(&a.tbits[v >> 5], ~bit);
+}
+
 // Finish one deterministic evaluation (thread-per-vertex flavour).
 __device__ __forceinline__ void det_commit_output(const SweepArgs &a, int32_t v, int32_t cur, int32_t cand, bool T,
                                                   int64_t lo, int64_t hi) {
     bool chg = T && cand != cur && (!a.pickless || cand < cur);
+    record_turn(a, v, T);
     uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
     uint32_t ow = __ldcg(&a.lab_new[v]);
     if (nw != ow) {
@@ -158,6 +170,7 @@ __device__ __forceinline__ void warp_hi_finish(const SweepArgs &a, int32_t v, in
         bool T = f0 != 0;
         if (!T) T = a.symmetric ? __any_sync(0xffffffffu, lower_changed) : lower_in_changed(a, v);
         bool chg = T && cand != cur && (!a.pickless || cand < cur);
+        if (lane == 0) record_turn(a, v, T);
         uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
         uint32_t ow = __ldcg(&a.lab_new[v]);
         __syncwarp();
@@ -531,6 +544,7 @@ __device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t
     if (go) {
         if (DET) {
             const bool chg = T && cand != cur && (!a.pickless || cand < cur);
+            record_turn(a, v, T);
             const uint32_t nw = chg ? ((uint32_t)cand | SLPA_CHG) : (uint32_t)cur;
             if (nw != __ldcg(&a.lab_new[v])) {
                 __stcg(&a.lab_new[v], nw);
@@ -586,12 +600,14 @@ struct MgLane {
     static constexpr bool kHasRescan = true;
     MgSketchDev<K, V> S, part;
     int k, p;
+    int32_t z;
     int64_t base, rem, next;
-    __device__ __forceinline__ void init(int k_, int32_t, int64_t deg, int P) {
+    __device__ __forceinline__ void init(int k_, int32_t, int64_t deg, int P, int32_t z_) {
         k = K > 0 ? K : k_;
-        S.reset(k);
+        z = z_;
+        S.reset(k, z);
         if (CHUNKED) {
-            part.reset(k);
+            part.reset(k, z);
             p = 0;
             base = deg / P;
             rem = deg % P;
@@ -609,7 +625,7 @@ struct MgLane {
                 if (pv > (V)0) S.acc(part.key[i], pv, k);
             }
         }
-        part.reset(k);
+        part.reset(k, z);
         ++p;
         next += base + (p < rem ? 1 : 0);
     }
@@ -643,7 +659,7 @@ struct BmLane {
     int32_t cur0;
     int p;
     int64_t base, rem, next;
-    __device__ __forceinline__ void init(int, int32_t cur, int64_t deg, int P) {
+    __device__ __forceinline__ void init(int, int32_t cur, int64_t deg, int P, int32_t) {
         cur0 = cur;
         st = BmVote<V>{cur, (V)0};
         if (CHUNKED) {
@@ -699,7 +715,7 @@ __global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int
         cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     }
     Pol pol;
-    pol.init(a.k, cur, deg, a.parts);
+    pol.init(a.k, cur, deg, a.parts, a.zkey);
     bool lower_changed = false;
     window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, lower_changed,
                                   [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
@@ -741,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, SLPA_LO_MINB) k_lane_direct(SweepArg
         cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     }
     Pol pol;
-    pol.init(a.k, cur, deg, a.parts);
+    pol.init(a.k, cur, deg, a.parts, a.zkey);
     bool lower_changed = false;
     // Rows of a warp have similar lengths (degree-ordered bins).  Short rows
     // stream unaligned -- element j of every lane is arc j of its own row, so
@@ -829,11 +845,11 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_direct(SweepArgs a, const in
     const int k = K > 0 ? K : a.k;
     const int P = a.parts;
     bool lower_changed = false;
-    WarpSketch<V> S_{0, (V)0};
+    WarpSketch<V> S_{a.zkey, (V)0, a.zkey};
     for (int b0 = 0; b0 < P; b0 += 32) {
         const int p = b0 + lane;
         MgSketchDev<K, V> part;
-        part.reset(k);
+        part.reset(k, a.zkey);
         int64_t cs = 0, ce = 0;
         if (p < P) chunk_bounds(deg, P, p, cs, ce);
         lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lower_changed, [&](int64_t, bool valid, int32_t c, W w) {
@@ -925,7 +941,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const
         hi[j] = __ldg(&a.off[v + 1]);
         cur[j] = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
         MgSketchDev<8, V> part;
-        part.reset(8);
+        part.reset(8, a.zkey);
         int64_t cs = 0, ce = 0;
         if (lane < P) chunk_bounds(hi[j] - lo[j], P, lane, cs, ce);
         bool lc = false;
@@ -951,7 +967,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const
             if (!__any_sync(0xffffffffu, live)) continue;
             const int32_t c = (int32_t)e.x;
             const V w = (V)e.y;
-            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c)) >> gb) & 0xffu;
+            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c, a.zkey)) >> gb) & 0xffu;
             const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
             const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
             const V d = (mm | fm) ? (V)0 : w;
@@ -1014,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
     const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
     const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     MgSketchDev<8, V> part;
-    part.reset(8);
+    part.reset(8, a.zkey);
     int64_t cs = 0, ce = 0;
     if (lane < a.parts) chunk_bounds(hi - lo, a.parts, lane, cs, ce);
     bool lc = false;
@@ -1048,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_merge(SweepArgs a, const int
     if (!(meta.y & 1u)) return;
     const uint32_t *src = a.hparts + (size_t)idx * kLpmWords;
     MgSketchDev<8, V> S;
-    S.reset(8);
+    S.reset(8, a.zkey);
     uint32_t kk[8], vv[8], kn[8], vn[8];
     ld8(src, kk);
     ld8(src + 256, vv);
@@ -1136,7 +1152,7 @@ __device__ __forceinline__ void group_chunk_scan(const SweepArgs &a, int64_t sta
                     lc |= live && (Lj >> 31) != 0;
                     const int32_t c = (int32_t)(Lj & SLPA_LMASK);
                     const V w = (V)wj;
-                    const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c)) >> gb) & 0xffu;
+                    const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c, a.zkey)) >> gb) & 0xffu;
                     const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
                     const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
                     const V d0 = (mm | fm) ? (V)0 : w;
@@ -1195,7 +1211,7 @@ __global__ void __launch_bounds__(kGiantWarps * 32) k_mg_hi_block(SweepArgs a, c
     const int lc_any = __syncthreads_or(lc ? 1 : 0);
     if (wib != 0) return;
     const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-    WarpSketch<V> S_{kNoKey, (V)0};
+    WarpSketch<V> S_{kNoKey, (V)0, a.zkey};
     if (lane < 8) {
         S_.key = s_key[0][lane];
         S_.val = s_val[0][lane];
@@ -1235,7 +1251,7 @@ __global__ void __launch_bounds__(kThreads) k_lo_warp(SweepArgs a, const int32_t
     const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
     const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     const int k = a.k;
-    WarpSketch<V> S_{kNoKey, (V)0};
+    WarpSketch<V> S_{kNoKey, (V)0, a.zkey};
     BmVote<V> st{cur, (V)0};
     bool lc = false;
     for (int pass = 0; pass < (!BM && a.scan_double ? 2 : 1); ++pass) {
@@ -1354,11 +1370,11 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const in
     const int k = K > 0 ? K : a.k;
     const int P = a.parts;
     bool lower_changed = false;
-    WarpSketch<V> S_{0, (V)0};
+    WarpSketch<V> S_{a.zkey, (V)0, a.zkey};
     for (int b0 = 0; b0 < P; b0 += 32) {
         const int p = b0 + lane;
         MgSketchDev<K, V> part;
-        part.reset(k);
+        part.reset(k, a.zkey);
         int64_t cs = 0, ce = 0;
         if (p < P) chunk_bounds(deg, P, p, cs, ce);
         window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
@@ -1571,11 +1587,11 @@ __global__ void __launch_bounds__(kWinThreads) k_mg_giant(SweepArgs a, const int
     const int k = K > 0 ? K : a.k;
     const int P = a.parts;
     bool lower_changed = false;
-    WarpSketch<V> S_{0, (V)0};
+    WarpSketch<V> S_{a.zkey, (V)0, a.zkey};
     for (int b0 = 0; b0 < P; b0 += 32) {
         const int p = b0 + lane;
         MgSketchDev<K, V> part;
-        part.reset(k);
+        part.reset(k, a.zkey);
         int64_t cs = 0, ce = 0;
         if (p < P) chunk_bounds(deg, P, p, cs, ce);
         giant_stream<W>(a, base + cs, base + ce, lower_changed, [&](int32_t c, W w) { part.acc(c, (V)w, k); });
@@ -1669,7 +1685,7 @@ __global__ void __launch_bounds__(kGiantWarps * 32) k_mg_giant_grp(SweepArgs a, 
             lc |= live && (Lj >> 31) != 0;
             const int32_t c = (int32_t)(Lj & SLPA_LMASK);
             const V w = (V)wj;
-            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c)) >> gb) & 0xffu;
+            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c, a.zkey)) >> gb) & 0xffu;
             const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
             const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
             const V d = (mm | fm) ? (V)0 : w;
@@ -1686,7 +1702,7 @@ __global__ void __launch_bounds__(kGiantWarps * 32) k_mg_giant_grp(SweepArgs a, 
     }
     const int lc_any = __syncthreads_or(lc ? 1 : 0);
     if (wib != 0) return;
-    WarpSketch<V> S_{kNoKey, (V)0};
+    WarpSketch<V> S_{kNoKey, (V)0, a.zkey};
     if (lane < 8) {
         S_.key = s_key[0][lane];
         S_.val = s_val[0][lane];
@@ -1745,62 +1761,225 @@ __global__ void __launch_bounds__(kWinThreads) k_bm_giant(SweepArgs a, const int
 }
 
 // ================================================================== exact
-// select_label_exact (lpa.py:92-107): per-label totals summed in adjacency
-// order (np.bincount order), argmax = smallest label among ties.  One thread
-// per vertex, O(deg^2) -- the correctness path for the quality baseline.
+// ------------------------------------------------------------------ exact variant
+// select_label_exact (lpa.py:92-107): totals = np.bincount(labels[nb],
+// weights) -- every label's weights summed in ARC order in binary64 -- then
+// argmax (largest total, the smallest label on ties).  A warp per vertex
+// walks the row in order, 32 arcs at a time; each arc finds its label's slot
+// in the warp's open-addressing table (global scratch, xcap slots, labels
+// inserted with atomicCAS); the lanes holding the same slot form a group
+// (match_any) and the group's lowest lane adds the members' weights one at a
+// time in lane (= arc) order, so every label's total sees exactly
+// bincount's sequence of additions.  O(deg) per vertex; the table is
+// cleared behind the vertex.
 template <class W, bool DET>
-__global__ void __launch_bounds__(kThreads) k_exact(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
-                                                    int round0) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long n_eval = 0, n_arcs = 0, n_delta = 0;
-    int32_t v = 0;
-    uint8_t f0 = 0;
-    bool go = false;
-    if (i < count) {
-        v = __ldg(&list[i]);
-        f0 = a.flag_cur[v];
-        go = DET ? (!round0 || f0) : (f0 != 0);
-    }
-    if (go) {
-        if (!DET) a.flag_cur[v] = 0;
+__global__ void __launch_bounds__(kThreads) k_exact_warp(SweepArgs a, const int32_t *__restrict__ list,
+                                                         int64_t count, int round0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = a.xunits;
+    if (gw >= nw) return;
+    const int64_t cap = a.xcap;  // power of two
+    int32_t *keys = reinterpret_cast<int32_t *>(a.xs) + (size_t)gw * (size_t)cap;
+    double *tot = reinterpret_cast<double *>(a.xs + (size_t)a.xunits * (size_t)cap * 4) + (size_t)gw * (size_t)cap;
+    for (int64_t idx = gw; idx < count; idx += nw) {
+        const int32_t v = __ldg(&list[idx]);
+        const uint8_t f0 = a.flag_cur[v];
+        const bool go = DET ? (!round0 || f0) : (f0 != 0);
+        if (!go) continue;  // warp-uniform
+        if (!DET) {
+            __syncwarp();
+            if (lane == 0) a.flag_cur[v] = 0;
+        }
         const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
         const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-        bool lower_changed = false, dummy = false;
+        bool lower_changed = false;
+        for (int64_t e0 = lo; e0 < hi; e0 += 32) {
+            const int64_t e = e0 + lane;
+            int32_t t = -1, c = -1;
+            double w = 0.0;
+            bool ok = false;
+            if (e < hi) {
+                t = __ldg(&a.tgt[e]);
+                ok = t != v;
+                if (ok) {
+                    if (DET) {
+                        const uint32_t L = gather_word<true>(a, t, v);
+                        lower_changed |= (L >> 31) != 0;
+                        c = (int32_t)(L & SLPA_LMASK);
+                    } else {
+                        c = __ldcg(&a.lab_old[t]);
+                    }
+                    w = arc_weight<W>(a, e);
+                }
+            }
+            int64_t slot = -1;
+            if (ok) {  // labels are non-negative; -1 marks an empty slot
+                int64_t h = (int64_t)(((uint32_t)c * 2654435761u) & (uint32_t)(cap - 1));
+                for (;;) {
+                    const int32_t old = atomicCAS(&keys[h], -1, c);
+                    if (old == -1 || old == c) break;
+                    h = (h + 1) & (cap - 1);
+                }
+                slot = h;
+            }
+            const unsigned grp = __match_any_sync(0xffffffffu, slot);
+            const bool leader = ok && lane == __ffs(grp) - 1;
+            double acc = leader ? __ldcg(&tot[slot]) : 0.0;
+            for (int b = 0; b < 32; ++b) {  // members in lane (= arc) order
+                const double wb = __shfl_sync(0xffffffffu, w, b);
+                if (leader && ((grp >> b) & 1u)) acc += wb;
+            }
+            if (leader) __stcg(&tot[slot], acc);
+            __syncwarp();
+        }
+        // argmax over the table (largest total, smallest label on ties), then clear it
+        double bw = 0.0;
+        int32_t bl = 0;
+        bool found = false;
+        for (int64_t h = lane; h < cap; h += 32) {
+            const int32_t k = __ldcg(&keys[h]);
+            if (k >= 0) {
+                const double x = __ldcg(&tot[h]);
+                if (!found || x > bw || (x == bw && k < bl)) { bw = x; bl = k; found = true; }
+                keys[h] = -1;
+                tot[h] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ow = __shfl_xor_sync(0xffffffffu, bw, o);
+            const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+            const int of = __shfl_xor_sync(0xffffffffu, (int)found, o);
+            if (of && (!found || ow > bw || (ow == bw && ol < bl))) { bw = ow; bl = ol; found = true; }
+        }
+        __syncwarp();
+        const int32_t cand = found ? bl : cur;  // no neighbour other than itself: the current label
+        warp_hi_finish<DET>(a, v, cur, cand, f0, lower_changed, lo, hi, lane);
+    }
+}
+
+// ------------------------------------------------------------------ large k
+// MgSketch with any slot count (sketch.py:17-137) for configurations the
+// register / slot-parallel sketches do not cover (k > 32 with chunked rows,
+// k > 64): a thread per vertex, its sketch and part sketch in global scratch
+// (slot i of unit u at [i * units + u], coalesced across the warp), the
+// reference's exact slot rules (first match incl. stale keys, first empty,
+// clamped decrement), chunks merged in order, optional double scan.  A
+// correctness path: one thread walks the whole row.
+template <class V>
+struct MgSketchMem {
+    int32_t *key;
+    V *val;
+    int64_t st;  // stride between slots
+    int k;
+    int32_t z;   // internal value of label 0
+    __device__ __forceinline__ void reset() {
+        for (int i = 0; i < k; ++i) { key[i * st] = kNoKey; val[i * st] = (V)0; }
+    }
+    __device__ __forceinline__ void acc(int32_t c, V w) {
+        for (int i = 0; i < k; ++i)
+            if (key_matches(key[i * st], c, z)) { key[i * st] = c; val[i * st] += w; return; }
+        for (int i = 0; i < k; ++i)
+            if (val[i * st] == (V)0) { key[i * st] = c; val[i * st] = w; return; }
+        for (int i = 0; i < k; ++i) val[i * st] = clamp_sub(val[i * st], w);
+    }
+    __device__ __forceinline__ void merge_from(const MgSketchMem &o) {  // sketch.py:76-91
+        for (int i = 0; i < k; ++i) {
+            const V x = o.val[i * o.st];
+            if (x > (V)0) acc(o.key[i * o.st], x);
+        }
+    }
+    __device__ __forceinline__ void clear_values() {
+        for (int i = 0; i < k; ++i) val[i * st] = (V)0;
+    }
+    __device__ __forceinline__ void rescan_add(int32_t c, V w) {
+        for (int i = 0; i < k; ++i)
+            if (key_matches(key[i * st], c, z)) { key[i * st] = c; val[i * st] += w; return; }
+    }
+    __device__ __forceinline__ bool max_key(int32_t &out) const {
         bool found = false;
         int32_t best = 0;
-        double bw = 0.0;
-        for (int64_t e1 = lo; e1 < hi; ++e1) {
-            int32_t t1 = __ldg(&a.tgt[e1]);
-            if (t1 == v) continue;
-            int32_t c1 = DET ? det_label(a, t1, v, lower_changed) : async_label(a, t1);
-            bool seen = false;
-            for (int64_t e0 = lo; e0 < e1 && !seen; ++e0) {
-                int32_t t0 = __ldg(&a.tgt[e0]);
-                if (t0 == v) continue;
-                int32_t c0 = DET ? det_label(a, t0, v, dummy) : async_label(a, t0);
-                seen = (c0 == c1);
+        V bw = (V)0;
+        for (int i = 0; i < k; ++i) {
+            const V x = val[i * st];
+            if (x > (V)0) {
+                const int32_t c = key[i * st];
+                if (!found || x > bw || (x == bw && c < best)) { best = c; bw = x; found = true; }
             }
-            if (seen) continue;
-            double tot = 0.0;
-            for (int64_t e2 = e1; e2 < hi; ++e2) {
-                int32_t t2 = __ldg(&a.tgt[e2]);
-                if (t2 == v) continue;
-                int32_t c2 = DET ? det_label(a, t2, v, dummy) : async_label(a, t2);
-                if (c2 == c1) tot += arc_weight<W>(a, e2);
-            }
-            if (!found || tot > bw || (tot == bw && c1 < best)) { best = c1; bw = tot; found = true; }
         }
-        const int32_t cand = found ? best : cur;
-        n_eval = 1;
-        n_arcs = (unsigned long long)(hi - lo);
+        out = best;
+        return found;
+    }
+};
+
+template <class W, bool DET, class V>
+__global__ void __launch_bounds__(kThreads) k_mg_bigk(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                      int round0) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nu = a.xunits;
+    if (u >= nu) return;
+    const int64_t U = a.xunits;
+    const int k = a.k;
+    int32_t *kbase = reinterpret_cast<int32_t *>(a.xs);
+    V *vbase = reinterpret_cast<V *>(a.xs + (size_t)U * (size_t)k * 2 * sizeof(int32_t));
+    MgSketchMem<V> S{kbase + u, vbase + u, U, k, a.zkey};
+    MgSketchMem<V> part{kbase + (int64_t)k * U + u, vbase + (int64_t)k * U + u, U, k, a.zkey};
+    for (int64_t idx = u; idx < count; idx += nu) {
+        const int32_t v = __ldg(&list[idx]);
+        const uint8_t f0 = a.flag_cur[v];
+        const bool go = DET ? (!round0 || f0) : (f0 != 0);
+        if (!go) continue;
+        if (!DET) a.flag_cur[v] = 0;
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        const int64_t deg = hi - lo;
+        const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
+        bool lower_changed = false;
+        auto label_of = [&](int32_t t) -> int32_t {
+            if (!DET) return __ldcg(&a.lab_old[t]);
+            const uint32_t L = gather_word<true>(a, t, v);
+            lower_changed |= (L >> 31) != 0;
+            return (int32_t)(L & SLPA_LMASK);
+        };
+        S.reset();
+        if (deg < a.thr || a.single) {  // lpa.py:172-176
+            for (int64_t e = lo; e < hi; ++e) {
+                const int32_t t = __ldg(&a.tgt[e]);
+                if (t != v) S.acc(label_of(t), (V)arc_weight<W>(a, e));
+            }
+        } else {  // lpa.py:177-186: parts[0] then merge(parts[1..]) in order
+            for (int r = 0; r < a.parts; ++r) {
+                int64_t cs, ce;
+                chunk_bounds(deg, a.parts, r, cs, ce);
+                MgSketchMem<V> &dst = r == 0 ? S : part;
+                if (r > 0) part.reset();
+                for (int64_t e = lo + cs; e < lo + ce; ++e) {
+                    const int32_t t = __ldg(&a.tgt[e]);
+                    if (t != v) dst.acc(label_of(t), (V)arc_weight<W>(a, e));
+                }
+                if (r > 0) S.merge_from(part);
+            }
+        }
+        if (a.scan_double) {  // lpa.py:187-191
+            S.clear_values();
+            for (int64_t e = lo; e < hi; ++e) {
+                const int32_t t = __ldg(&a.tgt[e]);
+                if (t != v) S.rescan_add(label_of(t), (V)arc_weight<W>(a, e));
+            }
+        }
+        int32_t best;
+        const int32_t cand = (deg > 0 && S.max_key(best)) ? best : cur;
+        unsigned long long n_delta = 0;
         if (DET) {
-            bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
+            const bool T = f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v));
             det_commit_output(a, v, cur, cand, T, lo, hi);
         } else {
             async_commit_output(a, v, cur, cand, lo, hi, n_delta);
+            if (n_delta) ctr_add(a.counters, CNT_DELTA, 1ull);
         }
+        ctr_add(a.counters, CNT_EVALS, 1ull);
+        ctr_add(a.counters, CNT_ARCS, (unsigned long long)deg);
     }
-    warp_count(a.counters, n_eval, n_arcs, n_delta);
 }
 
 int hi_grp_mode() {
@@ -1825,8 +2004,18 @@ int giant_grp_mode() {
 // execution path stays covered by the parity matrix (tests/test_gpu_paths.py).
 template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
-    if (cfg->variant == SLPA_VARIANT_EXACT)
-        return {k_exact<W, DET>, k_exact<W, DET>, k_exact<W, DET>, nullptr, nullptr, kThreads, kThreads, 0, 0, nullptr, nullptr, nullptr};
+    if (cfg->variant == SLPA_VARIANT_EXACT) {
+        KernelSet ks{k_exact_warp<W, DET>, k_exact_warp<W, DET>, k_exact_warp<W, DET>, nullptr, nullptr, kThreads,
+                     kThreads, 0, 0, nullptr, nullptr, nullptr};
+        ks.xmode = 1;
+        return ks;
+    }
+    if (slpa_large_k(cfg)) {
+        KernelSet ks{k_mg_bigk<W, DET, V>, k_mg_bigk<W, DET, V>, k_mg_bigk<W, DET, V>, nullptr, nullptr, kThreads,
+                     kThreads, 0, 0, nullptr, nullptr, nullptr};
+        ks.xmode = 2;
+        return ks;
+    }
     const bool direct = stage_mode() != 0;
     if (cfg->variant == SLPA_VARIANT_BM) {
         if (direct) {

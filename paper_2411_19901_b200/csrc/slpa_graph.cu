@@ -526,6 +526,7 @@ __global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const in
 void slpa_graph_finalize(slpa_ctx *ctx) {
     DeviceGraph &g = ctx->g;
     cudaStream_t s = ctx->stream;
+    g.max_deg = -1;
     g.bin_thr = -1;
     g.bin_single = -1;
     g.bin_lo_sorted = -1;
@@ -551,6 +552,7 @@ void slpa_graph_finalize(slpa_ctx *ctx) {
     CUDA_TRY(cudaStreamSynchronize(s));
     acc.release();
     g.symmetric = (h[0] == h[1]) && (h[2] == h[3]);
+    g.max_deg = (int64_t)h[6];
     // integer sketch values need integral weights and every weighted degree
     // < 2^31: max weight x max degree < 2^31 settles it; otherwise the exact
     // per-row sums decide
@@ -664,7 +666,8 @@ static int64_t hi_split() {
 void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg) {
     DeviceGraph &g = ctx->g;
     cudaStream_t s = ctx->stream;
-    const int single = (cfg->variant == SLPA_VARIANT_EXACT) || (cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch);
+    const int single = (cfg->variant == SLPA_VARIANT_EXACT) || (cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch) ||
+                       slpa_large_k(cfg);
     // deterministic mode: degree-sorted low bin (homogeneous warps); async
     // mode: ascending positions (closest to the sequential visiting order,
     // which async quality depends on)

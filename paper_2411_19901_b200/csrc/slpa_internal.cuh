@@ -106,6 +106,11 @@ struct SweepArgs {
     void *gw;                         // gathered weights (W)
     uint32_t *hparts;                 // high degree, lane-parallel merge: part sketches per worklist entry
     uint2 *hmeta;                     //   (cur label, active | f0 << 1 | lower_changed << 2) per entry
+    uint32_t *tbits;                  // profiling only (else null): bit v = v's last evaluation took its turn
+    unsigned char *xs;                // per-unit scratch of the exact / large-k kernels (xmode != 0)
+    int64_t xcap;                     //   exact: hash-table slots per warp; large k: unused
+    int64_t xunits;                   //   scratch units (threads or warps) the launch may use
+    int32_t zkey;                     // internal value of label 0 (0 unless caller labels were remapped)
 };
 
 enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_GIANT = 8, CNT_GPEND = 9, CNT_N = 10 };
@@ -145,6 +150,7 @@ struct DeviceGraph {
     DevBuf<int32_t> sort_v;
     int64_t n_lo = 0, n_mid = 0, n_hi = 0, n_giant = 0, giant_arcs = 0, giant_max_deg = 0;
     int64_t lo_max_deg = 0;  // largest degree in the low bin
+    int64_t max_deg = -1;    // largest degree (-1: not computed for this graph)
     const Csr &act() const { return has_order ? perm : base; }
     const int64_t *off() const { return act().off.p; }
     const int32_t *tgt() const { return act().tgt.p; }
@@ -163,6 +169,7 @@ struct WorkBuffers {
     DevBuf<uint32_t> dirty_a, dirty_b;
     DevBuf<uint32_t> dirty_g, dirty_gp;  // asynchronous giants: their marks / marks waiting for them
     DevBuf<uint8_t> dirty_bytes;  // multi-GPU deterministic: dirty marks exchanged as bytes
+    DevBuf<uint32_t> tbits;       // profiling: turn bitmap (the sequential sweep's processed set)
     DevBuf<unsigned long long> dcount;
     DevBuf<int32_t> wl_lo, wl_mid, wl_hi, wl_giant;
     DevBuf<uint32_t> hparts;      // lane-parallel merge scratch (high degree)
@@ -175,10 +182,11 @@ struct WorkBuffers {
     DevBuf<double> metric_d;    // tallies for modularity
     DevBuf<unsigned long long> metric_u;
     DevBuf<unsigned char> scratch;  // cub temp storage
+    DevBuf<unsigned char> xscratch; // exact / large-k kernels: per-warp hash tables or per-thread sketches
     size_t bytes() const {
         return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() + dirty_g.bytes() + dirty_gp.bytes() +
-               dirty_b.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
-               counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes();
+               dirty_b.bytes() + tbits.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
+               counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes() + xscratch.bytes();
     }
 };
 
@@ -202,6 +210,13 @@ struct slpa_ctx {
     cudaEvent_t gev0 = nullptr, gev1 = nullptr;
     int32_t giant_pending = 0;
     int32_t have_labels = 0;   // lab_old holds labels of a finished run
+    const slpa_config *cur_cfg = nullptr;  // configuration of the sweep being run
+    // caller label values -> internal (slpa_labels_from_host): 0 identity, 1 shift, 2 rank table
+    int32_t lmap_mode = 0;
+    int64_t lmap_shift = 0, lmap_n = 0;
+    DevBuf<int32_t> lmap_table;
+    int32_t zkey = 0;  // internal value of label 0
+    int64_t xs_key = 0, xs_units = 0;      // layout of wb.xscratch (exact table size or -k; units)
     int32_t l2_saved = 0;      // set_label_l2_window changed the process's persisting set-aside
     size_t l2_prev_limit = 0;  //   ... which was this before
     // multi-GPU partition
@@ -224,6 +239,8 @@ struct KernelSet {
     EvalKernel hi_finish;  //   and this one (a warp per vertex) commits the merged candidates
     EvalKernel hi_small;   // small high-degree rounds: fused block-per-vertex kernel
     EvalKernel lo_small;   // small low-degree rounds: warp per vertex
+    int xmode;             // 0; 1: `lo` is the exact warp-per-vertex kernel (hash table per warp);
+                           // 2: `lo` is the large-k thread-per-vertex kernel (two sketches per thread)
 };
 
 // slpa_eval_<weights>_<sketch values>_<mode>.cu
@@ -235,6 +252,13 @@ KernelSet slpa_pick_f64_u32_det(const slpa_config *cfg);
 KernelSet slpa_pick_f64_u32_async(const slpa_config *cfg);
 KernelSet slpa_pick_f64_f64_det(const slpa_config *cfg);
 KernelSet slpa_pick_f64_f64_async(const slpa_config *cfg);
+
+// MG configurations beyond the register / warp sketches (k > 32 with chunked
+// rows, or k > 64): every vertex runs the large-k kernel from the single bin.
+static inline bool slpa_large_k(const slpa_config *cfg) {
+    return cfg->variant == SLPA_VARIANT_MG && (cfg->shared_sketch ? cfg->sketch_slots > SLPA_KDYN
+                                                                  : cfg->sketch_slots > SLPA_KHI_MAX);
+}
 
 // ---------------------------------------------------------------- host-side helpers
 void slpa_validate_config(const slpa_config *cfg);

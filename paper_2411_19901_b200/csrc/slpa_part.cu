@@ -59,6 +59,7 @@ void mark_partitioned(slpa_ctx *ctx, int64_t vb, int64_t ve) {
     g.rsrc.release();
     g.symmetric = 1;  // only the asynchronous sweep runs partitioned
     slpa_check_int_weights(ctx);
+    g.max_deg = -1;
     g.bin_thr = -1;
     g.bin_single = -1;
     g.bin_lo_sorted = -1;

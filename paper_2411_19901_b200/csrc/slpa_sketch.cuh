@@ -40,7 +40,9 @@ __device__ __forceinline__ V clamp_sub(V v, V w) {  // max(v - w, 0) as sketch.p
 // identical to the reference's.
 constexpr int32_t kNoKey = -1;
 
-__device__ __forceinline__ bool key_matches(int32_t key, int32_t c) { return key == c || (c == 0 && key < 0); }
+// z: the internal value of label 0 -- 0, unless caller labels were remapped
+// (negative labels, slpa_labels_from_host), when it is the image of 0.
+__device__ __forceinline__ bool key_matches(int32_t key, int32_t c, int32_t z) { return key == c || (c == z && key < 0); }
 
 // MgSketch (sketch.py:17-137).  K > 0: compile-time slots (registers);
 // K == 0: runtime k <= SLPA_KDYN (local memory).
@@ -48,8 +50,10 @@ template <int K, class V = double>
 struct MgSketchDev {
     int32_t key[KArr<K>::v];
     V val[KArr<K>::v];
+    int32_t z;  // internal value of label 0 (key_matches)
 
-    __device__ __forceinline__ void reset(int k) {  // MgSketch.__init__ sketch.py:34-39
+    __device__ __forceinline__ void reset(int k, int32_t z_ = 0) {  // MgSketch.__init__ sketch.py:34-39
+        z = z_;
         if constexpr (K > 0) {
 #pragma unroll
             for (int i = 0; i < K; ++i) { key[i] = kNoKey; val[i] = (V)0; }
@@ -63,7 +67,7 @@ struct MgSketchDev {
     // every slot loses w, clamped at 0.
     __device__ __forceinline__ void acc(int32_t c, V w, int k) {
         if constexpr (K > 0) {
-            if (c != 0) {
+            if (c != z) {
                 // fast path: the key is unique, so "first match" is "the match"
                 bool any = false;
 #pragma unroll
@@ -90,7 +94,7 @@ struct MgSketchDev {
             unsigned mm = 0, fm = 0;
 #pragma unroll
             for (int i = 0; i < K; ++i) {
-                mm |= key_matches(key[i], c) ? (1u << i) : 0u;
+                mm |= key_matches(key[i], c, z) ? (1u << i) : 0u;
                 fm |= val[i] == (V)0 ? (1u << i) : 0u;
             }
             if (mm) {
@@ -109,7 +113,7 @@ struct MgSketchDev {
             }
         } else {
             for (int i = 0; i < k; ++i)
-                if (key_matches(key[i], c)) { key[i] = c; val[i] += w; return; }
+                if (key_matches(key[i], c, z)) { key[i] = c; val[i] += w; return; }
             for (int i = 0; i < k; ++i)
                 if (val[i] == (V)0) { key[i] = c; val[i] = w; return; }
             for (int i = 0; i < k; ++i) val[i] = clamp_sub(val[i], w);
@@ -136,14 +140,14 @@ struct MgSketchDev {
         if constexpr (K > 0) {
             unsigned mm = 0;
 #pragma unroll
-            for (int i = 0; i < K; ++i) mm |= key_matches(key[i], c) ? (1u << i) : 0u;
+            for (int i = 0; i < K; ++i) mm |= key_matches(key[i], c, z) ? (1u << i) : 0u;
             const unsigned sel = mm & (0u - mm);
 #pragma unroll
             for (int i = 0; i < K; ++i)
                 if (sel & (1u << i)) { key[i] = c; val[i] += w; }
         } else {
             for (int i = 0; i < k; ++i)
-                if (key_matches(key[i], c)) { key[i] = c; val[i] += w; return; }
+                if (key_matches(key[i], c, z)) { key[i] = c; val[i] += w; return; }
         }
     }
 
@@ -194,9 +198,9 @@ struct MgSketchDev<8, uint32_t> {
     uint32_t s[8];
     uint32_t D;
 
-    __device__ __forceinline__ void reset(int) {  // MgSketch.__init__ sketch.py:34-39
+    __device__ __forceinline__ void reset(int, int32_t z = 0) {  // MgSketch.__init__ sketch.py:34-39
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { key[i] = 0; s[i] = 0u; }
+        for (int i = 0; i < 8; ++i) { key[i] = z; s[i] = 0u; }  // every key starts as label 0
         D = 0u;
     }
     __device__ __forceinline__ uint32_t value(int i) const { return s[i] > D ? s[i] - D : 0u; }
@@ -324,9 +328,10 @@ template <class V = double>
 struct WarpSketch {
     int32_t key;
     V val;
+    int32_t z;  // internal value of label 0
     __device__ __forceinline__ void acc(int lane, int k, int32_t c, V w) {
         const bool live = lane < k;
-        const unsigned mm = __ballot_sync(0xffffffffu, live && key_matches(key, c));
+        const unsigned mm = __ballot_sync(0xffffffffu, live && key_matches(key, c, z));
         const unsigned fm = __ballot_sync(0xffffffffu, live && val == (V)0);
         if (mm) {
             if (lane == __ffs(mm) - 1) { key = c; val += w; }
@@ -337,7 +342,7 @@ struct WarpSketch {
         }
     }
     __device__ __forceinline__ void rescan_add(int lane, int k, int32_t c, V w) {
-        unsigned mm = __ballot_sync(0xffffffffu, lane < k && key_matches(key, c));
+        unsigned mm = __ballot_sync(0xffffffffu, lane < k && key_matches(key, c, z));
         if (mm && lane == __ffs(mm) - 1) { key = c; val += w; }
     }
     // max_key over the lanes; result valid on every lane.

@@ -20,6 +20,7 @@
 //     gather of a lower neighbour gives its label and whether it changed.
 // Async mode (worker_count > 0) is the paper's in-place parallel sweep.
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstring>
 #include <thread>
@@ -302,6 +303,7 @@ KernelSet kernels_for(const slpa_ctx *ctx, const slpa_config *cfg, bool det) {
 }
 
 SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
+    ctx->cur_cfg = cfg;
     SweepArgs a{};
     DeviceGraph &g = ctx->g;
     a.off = g.off();
@@ -333,6 +335,8 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         return e ? atoi(e) : 1;
     }();
     a.stream = stream;
+    a.tbits = ctx->prof_on ? ctx->wb.tbits.p : nullptr;
+    a.zkey = ctx->zkey;
     a.giant_bin = g.bin_giant.p;
     a.giant_off = g.giant_off.p;
     a.glab = ctx->wb.glab.p;
@@ -393,18 +397,95 @@ void timed_launch(slpa_ctx *ctx, int cls, int nlaunch, F &&fn, cudaStream_t st =
                 (long long)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI] - a0));
 }
 
-void launch_lane(slpa_ctx *ctx, EvalKernel k, int threads, const SweepArgs &a, const int32_t *list, int64_t cnt,
-                 int round0, int cls, EvalKernel small = nullptr) {
+// Largest degree of the resident graph (exact / large-k scratch sizing).
+__global__ void k_max_degree(const int64_t *__restrict__ off, int64_t n, unsigned long long *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long d = i < n ? (unsigned long long)(__ldg(&off[i + 1]) - __ldg(&off[i])) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, d, o);
+        d = x > d ? x : d;
+    }
+    if ((threadIdx.x & 31) == 0 && d) atomicMax(out, d);
+}
+
+int64_t graph_max_degree(slpa_ctx *ctx) {
+    DeviceGraph &g = ctx->g;
+    if (g.max_deg >= 0) return g.max_deg;
+    WorkBuffers &wb = ctx->wb;
+    wb.dcount.alloc(2);
+    CUDA_TRY(cudaMemsetAsync(wb.dcount.p, 0, sizeof(unsigned long long), ctx->stream));
+    if (g.n > 0) k_max_degree<<<grid_for(g.n, kThreads), kThreads, 0, ctx->stream>>>(g.off(), g.n, wb.dcount.p);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, wb.dcount.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    g.max_deg = (int64_t)h;
+    return g.max_deg;
+}
+
+// Scratch of the exact (xmode 1: an open-addressing table of xcap slots per
+// warp -- keys, then binary64 totals) and large-k (xmode 2: two k-slot
+// sketches per thread) kernels.  A fixed number of units (warps / threads,
+// at most ~1 GiB) stride over the worklist, so the layout only changes with
+// the table size or k; the exact tables start empty (key -1, total 0.0) and
+// the kernel leaves them so.
+void setup_xscratch(slpa_ctx *ctx, const KernelSet &ks, const slpa_config *cfg, SweepArgs &a) {
+    const size_t budget = (size_t)1 << 30;
+    int64_t cap = 0;
+    size_t per_unit;
+    if (ks.xmode == 1) {
+        cap = 64;
+        while (cap < 2 * std::max<int64_t>(graph_max_degree(ctx), 1)) cap <<= 1;
+        per_unit = (size_t)cap * 12;
+    } else {
+        const size_t vb = ctx->g.int_weights ? 4 : 8;
+        per_unit = (size_t)cfg->sketch_slots * 2 * (4 + vb);
+    }
+    int64_t units = std::min<int64_t>((int64_t)ctx->num_sms * 64, (int64_t)(budget / per_unit));
+    units = std::max<int64_t>(32, units / 32 * 32);
+    const int64_t key = ks.xmode == 1 ? cap : -cfg->sketch_slots;
+    const size_t need = per_unit * (size_t)units;
+    if (ctx->xs_key != key || ctx->xs_units != units || ctx->wb.xscratch.count < need) {
+        ctx->wb.xscratch.alloc(need);
+        if (ks.xmode == 1) {
+            CUDA_TRY(cudaMemsetAsync(ctx->wb.xscratch.p, 0xff, (size_t)units * cap * 4, ctx->stream));
+            CUDA_TRY(cudaMemsetAsync(ctx->wb.xscratch.p + (size_t)units * cap * 4, 0, (size_t)units * cap * 8,
+                                     ctx->stream));
+        }
+        ctx->xs_key = key;
+        ctx->xs_units = units;
+    }
+    a.xs = ctx->wb.xscratch.p;
+    a.xcap = cap;
+    a.xunits = units;
+}
+
+void launch_lane(slpa_ctx *ctx, const KernelSet &ks, int which, const SweepArgs &a0, const int32_t *list, int64_t cnt,
+                 int round0, int cls, bool allow_small = false) {
     if (cnt <= 0) return;
+    const EvalKernel k = which == 0 ? ks.lo : ks.mid;
+    const int threads = ks.lo_threads;
+    if (ks.xmode) {
+        SweepArgs a = a0;
+        setup_xscratch(ctx, ks, ctx->cur_cfg, a);
+        const int64_t items = ks.xmode == 1 ? a.xunits * 32 : a.xunits;
+        timed_launch(ctx, cls, 1, [&] {
+            k<<<grid_for(items, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
+            CUDA_TRY(cudaGetLastError());
+        });
+        return;
+    }
+    const EvalKernel small = (allow_small && which == 0) ? ks.lo_small : nullptr;
     if (small && cnt <= lo_small_max()) {  // few vertices: a warp per vertex (latency, not volume)
         timed_launch(ctx, cls, 1, [&] {
-            small<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(a, list, cnt, round0);
+            small<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(a0, list, cnt, round0);
             CUDA_TRY(cudaGetLastError());
         });
         return;
     }
     timed_launch(ctx, cls, 1, [&] {
-        k<<<grid_for(cnt, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
+        k<<<grid_for(cnt, threads), threads, 0, ctx->stream>>>(a0, list, cnt, round0);
         CUDA_TRY(cudaGetLastError());
     });
 }
@@ -707,6 +788,37 @@ __global__ void k_fold_all(int32_t *lab_old, uint32_t *lab_new, int64_t n) {
     }
 }
 
+// Profiling: vertices the sequential sweep processed (turn bitmap) and their arcs.
+// Isolated vertices are never evaluated (no bin); the sequential sweep still
+// processes them when flagged (lpa.py:212-214).
+__global__ void k_count_turns(const uint32_t *__restrict__ tbits, const int64_t *__restrict__ off,
+                              const uint8_t *__restrict__ f0, int64_t n, unsigned long long *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long nv = 0, na = 0;
+    if (i * 32 < n) {
+        const uint32_t w = tbits[i];
+        for (int b = 0; b < 32 && i * 32 + b < n; ++b) {
+            const int64_t v = i * 32 + b;
+            const int64_t d = __ldg(&off[v + 1]) - __ldg(&off[v]);
+            if ((w >> b) & 1u) {
+                ++nv;
+                na += (unsigned long long)d;
+            } else if (d == 0 && f0[v]) {
+                ++nv;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nv += __shfl_xor_sync(0xffffffffu, nv, o);
+        na += __shfl_xor_sync(0xffffffffu, na, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (nv || na)) {
+        atomicAdd(&out[0], nv);
+        atomicAdd(&out[1], na);
+    }
+}
+
 __global__ void k_iota(int32_t *out, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = (int32_t)i;
@@ -742,8 +854,8 @@ void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickles
             launch_giant(ctx, ks, a, wb.wl_giant.p, g.n_giant, 1);
         }
         launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
-        launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+        launch_lane(ctx, ks, 1, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
+        launch_lane(ctx, ks, 0, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
     } else {
         unsigned long long *cur_lo = wb.counters.p + CNT_LO * CNT_STRIPES,
                            *cur_mid = wb.counters.p + CNT_MID * CNT_STRIPES,
@@ -764,8 +876,8 @@ void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickles
                       nhi = (int64_t)ctx->h_sum[CNT_HI], ngiant = (int64_t)ctx->h_sum[CNT_GIANT];
         launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK, ks.lo_small);
-        launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
+        launch_lane(ctx, ks, 0, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK, true);
+        launch_lane(ctx, ks, 1, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
     }
     giant_join(ctx);
     if (n > 0) k_dirty_bits_to_bytes<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, wb.dirty_bytes.p, n);
@@ -824,6 +936,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(wb.flag_b.p, 0, (size_t)n, s));
     for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
+    if (ctx->prof_on) CUDA_TRY(cudaMemsetAsync(wb.tbits.p, 0, (size_t)((n + 31) / 32) * sizeof(uint32_t), s));
     static const int defer = [] {
         const char *e = getenv("SLPA_DEFER");
         return e ? atoi(e) : 2;
@@ -846,7 +959,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             launch_giant(ctx, ks, a, wb.wl_giant.p, g.n_giant, 1);
         }
         launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
-        launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
+        launch_lane(ctx, ks, 1, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
     }
     // Round 0, light vertices: only the flagged entries of the degree-ordered
     // bin.  After sweep 0 a minority is flagged; launching the whole bin would
@@ -862,9 +975,9 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         unsigned long long nf = 0;
         CUDA_TRY(cudaMemcpyAsync(&nf, c0, sizeof(nf), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, (int64_t)nf, 1, SLPA_PROF_EVAL_LO0);
+        launch_lane(ctx, ks, 0, a, wb.wl_lo.p, (int64_t)nf, 1, SLPA_PROF_EVAL_LO0);
     } else {
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+        launch_lane(ctx, ks, 0, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
     }
     int64_t rounds = 1;
     unsigned long long evals0 = 0, arcs0 = 0;
@@ -1004,8 +1117,8 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
             launch_giant(ctx, ks, a, wb.wl_giant.p, ngiant, 0);
         }
         launch_hi(ctx, ks, a, wb.wl_hi.p, nhi, 0, SLPA_PROF_EVAL_HIK);
-        launch_lane(ctx, ks.lo, ks.lo_threads, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK, ks.lo_small);
-        launch_lane(ctx, ks.mid, ks.lo_threads, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
+        launch_lane(ctx, ks, 0, a, wb.wl_lo.p, nlo, 0, SLPA_PROF_EVAL_LOK, true);
+        launch_lane(ctx, ks, 1, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
         ++rounds;
     }
     giant_join(ctx);
@@ -1070,8 +1183,20 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     ctx->stats.rounds += rounds;
     ctx->stats.vertex_evals += (int64_t)evals;
     ctx->stats.arc_reads += (int64_t)arcs;
-    ctx->stats.first_evals += (int64_t)evals0;
-    ctx->stats.first_arcs += (int64_t)arcs0;
+    if (ctx->prof_on && n > 0) {  // the sequential sweep's processed set, from the turn bitmap
+        wb.dcount.alloc(2);
+        CUDA_TRY(cudaMemsetAsync(wb.dcount.p, 0, 2 * sizeof(unsigned long long), s));
+        const int64_t nw = (n + 31) / 32;
+        k_count_turns<<<grid_for(nw, kThreads), kThreads, 0, s>>>(wb.tbits.p, g.off(), wb.flag_b.p /* F0, swapped above */, n, wb.dcount.p);
+        CUDA_TRY(cudaGetLastError());
+        unsigned long long h[2] = {0, 0};
+        CUDA_TRY(cudaMemcpyAsync(h, wb.dcount.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        ctx->stats.first_evals += (int64_t)h[0];
+        ctx->stats.first_arcs += (int64_t)h[1];
+    }
+    (void)evals0;
+    (void)arcs0;
     return (int64_t)ctx->h_sum[CNT_DELTA];
 }
 
@@ -1089,8 +1214,8 @@ int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         launch_giant(ctx, ks, a, wb.wl_giant.p, g.n_giant, 1);
     }
     launch_hi(ctx, ks, a, g.bin_hi.p, g.n_hi, 1, SLPA_PROF_EVAL_HI0);
-    launch_lane(ctx, ks.mid, ks.lo_threads, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
-    launch_lane(ctx, ks.lo, ks.lo_threads, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+    launch_lane(ctx, ks, 1, a, g.bin_mid.p, g.n_mid, 1, SLPA_PROF_EVAL_MID0);
+    launch_lane(ctx, ks, 0, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
     giant_join(ctx);
     if (!ctx->part) {  // partitioned: remote entries hold outgoing marks, cleared after the exchange
         timed_launch(ctx, SLPA_PROF_OTHER, 1, [&] {
@@ -1109,7 +1234,94 @@ int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     return (int64_t)ctx->h_sum[CNT_DELTA];
 }
 
+// ------------------------------------------------------------------ caller label values
+// The kernels keep labels in 31 bits (bit 31 of lab_new is the changed
+// flag).  Caller labels (lpa_move, a hook that edits the live array) may be
+// any int32 (lpa.py:227-259).  The sweep only compares labels (equality,
+// order for pick-less sweeps and ties) and never creates new values, so an
+// order-preserving map of the label set into [0, 2^31) is exact: a shift by
+// the minimum when the span fits, else the rank in sorted(labels + {0}).
+// The sketches start every key as "label 0" (sketch.py:38) -- its image
+// under the map is SweepArgs::zkey.  Labels go back through the inverse.
+__global__ void k_minmax_i32(const int32_t *__restrict__ x, int64_t n, int *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int lo = INT_MAX, hi = INT_MIN;
+    if (i < n) lo = hi = x[i];
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&out[0], lo);
+        atomicMax(&out[1], hi);
+    }
+}
+__global__ void k_shift_i32(const int32_t *__restrict__ in, int32_t *__restrict__ out, int64_t n, int64_t d) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)((int64_t)in[i] + d);
+}
+__global__ void k_rank_i32(int32_t *__restrict__ x, int64_t n, const int32_t *__restrict__ table, int64_t nt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t v = x[i];
+    int64_t lo = 0, hi = nt - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(&table[mid]) < v) lo = mid + 1;
+        else hi = mid;
+    }
+    x[i] = (int32_t)lo;
+}
+__global__ void k_unrank_i32(const int32_t *__restrict__ in, int32_t *__restrict__ out, int64_t n,
+                             const int32_t *__restrict__ table) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __ldg(&table[in[i]]);
+}
+
+// lab_old (by position) holds raw caller labels: map them in place.
+void map_caller_labels(slpa_ctx *ctx, const int32_t *host_by_id) {
+    const int64_t n = ctx->g.n;
+    cudaStream_t s = ctx->stream;
+    ctx->lmap_mode = 0;
+    ctx->lmap_shift = 0;
+    ctx->zkey = 0;
+    WorkBuffers &wb = ctx->wb;
+    wb.dcount.alloc(2);
+    int *mm = reinterpret_cast<int *>(wb.dcount.p);
+    const int init[2] = {INT_MAX, INT_MIN};
+    CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    k_minmax_i32<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, n, mm);
+    CUDA_TRY(cudaGetLastError());
+    int h[2];
+    CUDA_TRY(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (h[0] >= 0) return;  // the common case: labels are already non-negative
+    const int64_t lo = h[0], hi = std::max<int64_t>(h[1], 0);
+    if (hi - lo < (int64_t)SLPA_LMASK) {  // shift by the minimum
+        ctx->lmap_mode = 1;
+        ctx->lmap_shift = lo;
+        ctx->zkey = (int32_t)(-lo);
+        k_shift_i32<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, wb.lab_old.p, n, -lo);
+        CUDA_TRY(cudaGetLastError());
+        return;
+    }
+    // rank in the sorted label set (plus 0, so label 0 has an image)
+    std::vector<int32_t> t(host_by_id, host_by_id + n);
+    t.push_back(0);
+    std::sort(t.begin(), t.end());
+    t.erase(std::unique(t.begin(), t.end()), t.end());
+    ctx->lmap_table.alloc(t.size());
+    CUDA_TRY(cudaMemcpyAsync(ctx->lmap_table.p, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    ctx->lmap_n = (int64_t)t.size();
+    ctx->lmap_mode = 2;
+    ctx->zkey = (int32_t)(std::lower_bound(t.begin(), t.end(), 0) - t.begin());
+    k_rank_i32<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, n, ctx->lmap_table.p, ctx->lmap_n);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));  // t is freed on return
+}
+
 void slpa_init_labels(slpa_ctx *ctx) {
+    ctx->lmap_mode = 0;
+    ctx->lmap_shift = 0;
+    ctx->zkey = 0;
     const int64_t n = ctx->g.n;
     if (n == 0) return;
     k_init_labels<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(
@@ -1121,6 +1333,16 @@ void slpa_labels_to_host(slpa_ctx *ctx, int32_t *host) {
     const int64_t n = ctx->g.n;
     if (n == 0) return;
     const int32_t *src = ctx->wb.lab_old.p;
+    DevBuf<int32_t> unmapped;
+    if (ctx->lmap_mode) {  // back to the caller's label values
+        unmapped.alloc(n);
+        if (ctx->lmap_mode == 1)
+            k_shift_i32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(src, unmapped.p, n, ctx->lmap_shift);
+        else
+            k_unrank_i32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(src, unmapped.p, n, ctx->lmap_table.p);
+        CUDA_TRY(cudaGetLastError());
+        src = unmapped.p;
+    }
     if (ctx->g.has_order) {
         k_pos_to_id_i32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(src, ctx->wb.io_labels.p, ctx->g.ids.p, n);
         CUDA_TRY(cudaGetLastError());
@@ -1160,6 +1382,7 @@ void slpa_labels_from_host(slpa_ctx *ctx, const int32_t *host) {
     } else {
         CUDA_TRY(cudaMemcpyAsync(ctx->wb.lab_old.p, host, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
     }
+    map_caller_labels(ctx, host);
     k_sync_lab_new<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.lab_old.p, ctx->wb.lab_new.p, n);
     CUDA_TRY(cudaGetLastError());
 }

@@ -167,16 +167,20 @@ class Engine:
         c = config_struct(cfg)
         delta = np.zeros(max(int(cfg.max_iterations), 1), dtype=np.int64)
         iters, conv = ctypes.c_int32(0), ctypes.c_int32(0)
+        if hook is not None:
+            fetch_labels = True  # the hook sees the live result array
         labels = np.empty(max(self.n, 1), dtype=np.int32) if fetch_labels else None
+        live = labels[: self.n] if labels is not None else None
         err = []
         cb = HOOK_FN()
         if hook is not None:
-            n = self.n
+            # lpa.py:271-273, :297-298: the hook receives the live labels array --
+            # the same object every sweep and the one returned; the library
+            # writes it before the call and uploads any edit the hook makes.
 
             def _tramp(user, it, pickless, ptr):
                 try:
-                    arr = np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.empty(0, np.int32)
-                    hook(int(it), bool(pickless), arr)
+                    hook(int(it), bool(pickless), live)
                     return 0
                 except BaseException as e:  # re-raised after the C call returns
                     err.append(e)
@@ -189,9 +193,7 @@ class Engine:
             raise err[0]
         check(self.lib, self.ctx, rc)
         it = iters.value
-        if labels is not None:
-            labels = labels[: self.n]
-        return labels, it, [int(x) for x in delta[:it]], bool(conv.value)
+        return live, it, [int(x) for x in delta[:it]], bool(conv.value)
 
     def move(self, cfg, labels, unprocessed, pickless):
         """lpa_move on the resident graph; mutates labels/unprocessed in place."""

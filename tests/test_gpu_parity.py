@@ -109,6 +109,41 @@ def test_config_errors_raise_value_error(slpa, eng):
         slpa.lpa_run(g, slpa.LpaConfig(), order=np.array([0, 1]), engine=eng)
 
 
+@pytest.mark.parametrize("name", G.names(kind="run_mutating_hook"))
+def test_mutating_hook_vs_reference(slpa, eng, name):
+    """The hook receives the LIVE labels (lpa.py:271-273): an edit it makes
+    feeds the next sweep, and the array it saw is the one returned."""
+    g = G.graph(name)
+    meta = G.meta(name)
+    cfg = G.cfg(name, slpa.LpaConfig)
+    hist, seen = [], []
+
+    def hook(it, pickless, labels):
+        if it == 0:
+            labels[::7] = labels[0]
+        seen.append(labels)
+        hist.append(labels.copy())
+
+    res = slpa.lpa_run(g, cfg, iteration_hook=hook, engine=eng)
+    assert res.iterations == meta["iterations"]
+    assert res.delta_history == meta["delta_history"]
+    np.testing.assert_array_equal(res.labels, G.get(name, "labels"))
+    np.testing.assert_array_equal(np.stack(hist), G.get(name, "label_hist"))
+    assert all(x is res.labels for x in seen)
+
+
+@pytest.mark.parametrize("name", G.names(kind="move_raises"))
+def test_move_raises_like_reference(slpa, eng, name):
+    """exact + negative caller labels: np.bincount raises ValueError in the
+    reference (lpa.py:104); the drop-in raises the same type."""
+    g = G.graph(name)
+    cfg = G.cfg(name, slpa.LpaConfig)
+    labels = G.get(name, "in_labels").copy()
+    flags = G.get(name, "in_flags").astype(bool)
+    with pytest.raises(ValueError):
+        slpa.lpa_move(g, labels, flags, cfg, G.meta(name)["pickless"], engine=eng)
+
+
 def test_hook_exception_propagates(slpa, eng):
     g = slpa.build_graph(4, [(0, 1), (1, 2), (2, 3)], engine=eng)
 
@@ -197,12 +232,38 @@ def test_rmat_run_bit_exact_vs_oracle(slpa, eng, oracle, scale, ci):
     g = GoldenGraph(off, tgt, w)
     ref = oracle.lpa_run(g, cfg, keep_history=True)
     hist = []
-    labels, iters, delta, conv = eng.run(cfg, hook=lambda it, pl, lab: hist.append(lab))
+    labels, iters, delta, conv = eng.run(cfg, hook=lambda it, pl, lab: hist.append(lab.copy()))
     assert iters == ref.iterations
     assert delta == ref.delta_history
     assert conv == ref.converged
     np.testing.assert_array_equal(labels, ref.labels)
     np.testing.assert_array_equal(np.stack(hist), ref.label_history)
+
+
+@pytest.mark.parametrize("variant", ["mg", "bm"])
+@pytest.mark.parametrize("scale", [12, 16])
+def test_processed_set_counts_match_sequential_sweeps(slpa, eng, oracle, scale, variant):
+    """The run-level roofline's algorithmic work (bench.py run_frac): the
+    vertices the sequential sweeps process and their arcs, counted on the
+    device from the final evaluations' turn bits, equal the reference
+    sweep's own count (lpa.py:212-214)."""
+    eng.gen_rmat(scale, seed=31 + scale, permute=True)
+    off, tgt, w = eng.download()
+    from golden_io import GoldenGraph
+    g = GoldenGraph(off, tgt, w)
+    cfg = slpa.LpaConfig(variant=variant)
+    oracle.processed(reset=True)
+    ref = oracle.lpa_run(g, cfg)
+    pv, pa = oracle.processed()
+    eng.set_profiling(True)
+    try:
+        labels, iters, delta, conv = eng.run(cfg)
+        st = eng.stats()
+    finally:
+        eng.set_profiling(False)
+    assert (iters, delta) == (ref.iterations, ref.delta_history)
+    np.testing.assert_array_equal(labels, ref.labels)
+    assert (st["first_evals"], st["first_arcs"]) == (pv, pa)
 
 
 @pytest.mark.parametrize("kind", ["grid_rowmajor", "grid_perm", "kmer", "rmat_raw"])
