@@ -117,6 +117,7 @@ void slpa_alloc_work(slpa_ctx *ctx) {
     wb.io_flags.alloc(n);
     wb.counters.alloc(CNT_TOTAL);
     if (ctx->prof_on) wb.tbits.alloc(n / 32 + 1);
+    wb.fbits.alloc(n / 32 + 1);
     CUDA_TRY(cudaMemsetAsync(wb.dirty_a.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     CUDA_TRY(cudaMemsetAsync(wb.dirty_b.p, 0, (n / 32 + 1) * sizeof(uint32_t), ctx->stream));
     if (!ctx->h_counters) CUDA_TRY(cudaMallocHost((void **)&ctx->h_counters, CNT_TOTAL * sizeof(unsigned long long)));
@@ -252,7 +253,7 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
     wb.io_labels.release(); wb.io_flags.release(); wb.counters.release(); wb.metric_d.release();
     wb.metric_u.release(); wb.scratch.release();
     wb.hparts.release(); wb.hmeta.release(); wb.dirty_g.release(); wb.dirty_gp.release();
-    wb.dirty_bytes.release(); wb.dcount.release(); wb.tbits.release(); wb.xscratch.release();
+    wb.dirty_bytes.release(); wb.dcount.release(); wb.tbits.release(); wb.fbits.release(); wb.xscratch.release();
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     ctx->h_stage = nullptr;
     ctx->h_stage_n = 0;

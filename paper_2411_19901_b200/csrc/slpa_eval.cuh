@@ -197,125 +197,9 @@ __device__ __forceinline__ void warp_hi_finish(const SweepArgs &a, int32_t v, in
     }
 }
 
-// ================================================================== window staging
-// A warp runs 32 sequential streams (one per lane): 32 rows (low degree) or
-// the 32 chunks of one vertex (high degree).  For each window of S steps the
-// warp stages the next <= S arcs of every stream into a padded shared tile
-// [lane][step] -- the concatenated window is loaded with consecutive lanes on
-// consecutive arcs (coalesced targets / weights, 32 independent label
-// gathers per instruction) -- then every lane replays its own S steps in
-// order.  Self-arcs are staged with weight 0 (weights are > 0).
+// Warp-per-giant kernels (k_mg_giant, k_bm_giant) run 4-warp blocks.
 constexpr int kWinWarps = 4;
 constexpr int kWinThreads = kWinWarps * 32;
-
-template <class W>
-struct WinS {
-    static constexpr int S = sizeof(W) == 4 ? 32 : 16;
-};
-
-template <class W, bool DET, bool GRID, class Consume>
-__device__ __forceinline__ void window_streams(const SweepArgs &a, uint32_t (*s_lab)[WinS<W>::S + 1],
-                                               W (*s_w)[WinS<W>::S + 1], int lane, int64_t start, int64_t len,
-                                               int32_t sv, bool &lower_changed, Consume &&consume) {
-    constexpr int S = WinS<W>::S;
-    constexpr int G = 8;  // staging iterations in flight per lane
-    const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
-    const uint64_t pol = policy_evict_first();
-    int64_t maxlen = len;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        int64_t x = __shfl_xor_sync(0xffffffffu, maxlen, o);
-        maxlen = x > maxlen ? x : maxlen;
-    }
-    for (int64_t s0 = 0; s0 < maxlen; s0 += S) {
-        const int64_t rem = len - s0;
-        const int seg = rem <= 0 ? 0 : (rem >= S ? S : (int)rem);
-        int excl = 0, total = 0, iters;
-        if (GRID) {
-            // stream j's window is staged by iteration j, lane = step (coalesced)
-            iters = 32;
-        } else {
-            int incl = seg;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int x = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += x;
-            }
-            excl = incl - seg;
-            total = __shfl_sync(0xffffffffu, incl, 31);
-            iters = (total + 31) >> 5;
-        }
-        for (int j0 = 0; j0 < iters; j0 += G) {
-            int32_t t[G], ov[G];
-            W w[G];
-            int own[G], stp[G];
-            bool ok[G];
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-                const int j = j0 + u;
-                int o, sp;
-                bool valid;
-                if (GRID) {
-                    o = j & 31;
-                    sp = lane;
-                    const int sj = __shfl_sync(0xffffffffu, seg, o);
-                    valid = j < 32 && lane < sj;
-                } else {
-                    const int va = j * 32 + lane;
-                    o = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        int ex = __shfl_sync(0xffffffffu, excl, (o + step) & 31);
-                        if (o + step < 32 && ex <= va) o += step;
-                    }
-                    sp = va - __shfl_sync(0xffffffffu, excl, o);
-                    valid = va < total;
-                }
-                const int64_t o_start = __shfl_sync(0xffffffffu, start, o);
-                ov[u] = __shfl_sync(0xffffffffu, sv, o);
-                own[u] = o;
-                stp[u] = sp;
-                ok[u] = valid;
-                if (valid) {
-                    const int64_t e = o_start + s0 + sp;
-                    t[u] = ld_stream(&a.tgt[e], pol);
-                    w[u] = ld_stream(&wts[e], pol);
-                } else {
-                    t[u] = 0;
-                    w[u] = (W)0;
-                }
-            }
-            uint32_t L[G];
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-                L[u] = 0;
-                if (ok[u] && t[u] != ov[u]) L[u] = DET ? __ldcg(&a.lab_new[t[u]]) : (uint32_t)__ldcg(&a.lab_old[t[u]]);
-            }
-            if (DET) {  // higher neighbour that changed this sweep: its L0
-#pragma unroll
-                for (int u = 0; u < G; ++u)
-                    if (ok[u] && t[u] > ov[u] && (L[u] >> 31)) L[u] = (uint32_t)__ldg(&a.lab_old[t[u]]);
-            }
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-                if (ok[u]) {
-                    s_lab[own[u]][stp[u]] = L[u];
-                    s_w[own[u]][stp[u]] = (t[u] == ov[u]) ? (W)0 : w[u];
-                }
-            }
-        }
-        __syncwarp();
-#pragma unroll 4
-        for (int x = 0; x < seg; ++x) {
-            const W w = s_w[lane][x];
-            const uint32_t L = s_lab[lane][x];
-            const bool valid = w != (W)0;
-            lower_changed |= valid && (L >> 31) != 0;
-            consume(s0 + x, valid, (int32_t)(L & SLPA_LMASK), w);
-        }
-        __syncwarp();
-    }
-}
 
 // ================================================================== direct streaming
 // Every lane streams its own arc range [start, start + len) in 32-byte aligned
@@ -425,13 +309,18 @@ __device__ __forceinline__ void ld_batch_u(const SweepArgs &a, const W *__restri
     }
 }
 
+// The high-degree scans gather every word from lab_new, the array L2 keeps
+// resident (a higher neighbour's L0 is fetched from lab_old only when its
+// changed bit is set): at RMAT s24 reading lab_old directly for every higher
+// neighbour doubles the gathers' L2 footprint and measured 13.1 GB of DRAM
+// reads per first heavy launch instead of 5.6 GB.
 template <bool DET>
 __device__ __forceinline__ void gather_batch(const SweepArgs &a, int32_t v, const int32_t (&t)[kBatch],
                                              uint32_t (&L)[kBatch]) {
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
         L[j] = 0;
-        if (t[j] != v) L[j] = gather_word<DET>(a, t[j], v);
+        if (t[j] != v) L[j] = DET ? __ldcg(&a.lab_new[t[j]]) : (uint32_t)__ldcg(&a.lab_old[t[j]]);
     }
 }
 
@@ -449,6 +338,11 @@ __device__ __forceinline__ void lane_stream_p(const SweepArgs &a, int64_t start,
     for (int64_t x0 = 0;;) {
         gather_batch<DET>(a, v, tB, LB);                                // batch i+1 (masked past the end)
         ld_batch_u<W, DET>(a, wts, start, x0 + 2 * kBatch, len, v, tC, wC);  // batch i+2
+        if (DET) {  // higher neighbour that changed this sweep: its L0
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (tA[j] > v && (LA[j] >> 31)) LA[j] = (uint32_t)__ldg(&a.lab_old[tA[j]]);
+        }
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             if (x0 + j < len) {
@@ -520,15 +414,6 @@ __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, i
             w[j] = wn[j];
         }
     }
-}
-
-// Stage selection: 1 = direct streaming (default), 0 = window staging.
-int stage_mode() {
-    static const int m = [] {
-        const char *e = getenv("SLPA_STAGE");
-        return e ? atoi(e) : 1;
-    }();
-    return m;
 }
 
 // ================================================================== lane kernels
@@ -690,52 +575,7 @@ struct BmLane {
     __device__ __forceinline__ int32_t result(int32_t) const { return best.cand; }
 };
 
-template <class W, class Pol, bool DET>
-__global__ void __launch_bounds__(kWinThreads) k_lane_win(SweepArgs a, const int32_t *__restrict__ list,
-                                                          int64_t count, int round0) {
-    constexpr int S = WinS<W>::S;
-    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
-    __shared__ W s_w[kWinWarps][32][S + 1];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int32_t v = -1;
-    uint8_t f0 = 0;
-    bool go = false;
-    if (i < count) {
-        v = __ldg(&list[i]);
-        f0 = a.flag_cur[v];
-        go = DET ? (!round0 || f0) : (f0 != 0);
-    }
-    int64_t lo = 0, deg = 0;
-    int32_t cur = 0;
-    if (go) {
-        if (!DET) a.flag_cur[v] = 0;
-        lo = __ldg(&a.off[v]);
-        deg = __ldg(&a.off[v + 1]) - lo;
-        cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-    }
-    Pol pol;
-    pol.init(a.k, cur, deg, a.parts, a.zkey);
-    bool lower_changed = false;
-    window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, lower_changed,
-                                  [&](int64_t pos, bool valid, int32_t c, W w) { pol.on(pos, valid, c, w); });
-    if (go && deg) pol.finish();
-    if (Pol::kHasRescan && a.scan_double) {
-        pol.rescan_begin();
-        bool dummy = false;
-        window_streams<W, DET, false>(a, s_lab[wib], s_w[wib], lane, lo, deg, v, dummy,
-                                      [&](int64_t, bool valid, int32_t c, W w) {
-                                          if (valid) pol.rescan(c, w);
-                                      });
-    }
-    unsigned long long n_delta = 0;
-    const int32_t cand = (go && deg) ? pol.result(cur) : cur;
-    const bool T = go && (f0 || (a.symmetric ? lower_changed : lower_in_changed(a, v)));
-    lane_finish<DET>(a, go, v, cur, cand, T, lo, deg, n_delta);
-    warp_count(a.counters, go ? 1ull : 0ull, (unsigned long long)deg, n_delta);
-}
-
-// Same evaluation as k_lane_win, every lane streaming its own row directly.
+// One lane per vertex, every lane streaming its own row directly.
 template <class W, class Pol, bool DET>
 __global__ void __launch_bounds__(kThreads, SLPA_LO_MINB) k_lane_direct(SweepArgs a, const int32_t *__restrict__ list,
                                                           int64_t count, int round0) {
@@ -887,117 +727,6 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_direct(SweepArgs a, const in
     warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
 }
 
-// High degree, MG, k = 8, R_H <= 32: a warp evaluates kGrp vertices.
-//  (A) per vertex, lane g streams chunk g into a register part sketch and
-//      stores it (physical slots: keys incl. stale ones, values) to shared
-//      memory;
-//  (B) the ordered merge sk = parts[0]; sk.merge(parts[1]); ...
-//      (lpa.py:179-186, sketch.py:76-91) runs for the kGrp vertices at once,
-//      one 8-lane group per vertex, lane = slot: every replayed (key, value)
-//      is one group-wise accumulate (first matching lane, else first empty
-//      lane, else every lane decrements) -- 4 merges for the instructions of
-//      one;
-//  (C) max_key per group, then the warp finishes the vertices one by one.
-constexpr int kGrp = 4;
-constexpr int kGrpWarps = 4;
-
-template <class W, bool DET, class V>
-__global__ void __launch_bounds__(kGrpWarps * 32) k_mg_hi_grp(SweepArgs a, const int32_t *__restrict__ list,
-                                                             int64_t count, int round0) {
-    static_assert(sizeof(V) == 4, "grouped merge packs (key, value) in 8 bytes");
-    __shared__ uint2 s_part[kGrpWarps][kGrp][32][8];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t first = wid * kGrp;
-    if (first >= count) return;  // warp-uniform
-    const int P = a.parts;
-    uint2(*sp)[32][8] = s_part[wib];
-    int32_t vv[kGrp], cur[kGrp];
-    int64_t lo[kGrp], hi[kGrp];
-    uint8_t f0[kGrp];
-    bool act[kGrp], lch[kGrp];
-#pragma unroll
-    for (int j = 0; j < kGrp; ++j) {
-        act[j] = false;
-        lch[j] = false;
-        vv[j] = 0;
-        cur[j] = 0;
-        lo[j] = hi[j] = 0;
-        f0[j] = 0;
-        if (first + j < count) {
-            vv[j] = __ldg(&list[first + j]);
-            f0[j] = a.flag_cur[vv[j]];
-            act[j] = DET ? !(round0 && !f0[j]) : f0[j] != 0;
-        }
-    }
-    __syncwarp();
-    // (A) chunk scans
-#pragma unroll
-    for (int j = 0; j < kGrp; ++j) {
-        if (!act[j]) continue;  // warp-uniform
-        const int32_t v = vv[j];
-        if (!DET && lane == 0) a.flag_cur[v] = 0;
-        lo[j] = __ldg(&a.off[v]);
-        hi[j] = __ldg(&a.off[v + 1]);
-        cur[j] = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-        MgSketchDev<8, V> part;
-        part.reset(8, a.zkey);
-        int64_t cs = 0, ce = 0;
-        if (lane < P) chunk_bounds(hi[j] - lo[j], P, lane, cs, ce);
-        bool lc = false;
-        lane_stream_u<W, DET>(a, lo[j] + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
-            if (valid) part.acc(c, (V)w, 8);
-        });
-        lch[j] = __any_sync(0xffffffffu, lc);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sp[j][lane][i] = make_uint2((uint32_t)part.key[i], (uint32_t)part.value(i));
-    }
-    __syncwarp();
-    // (B) grouped ordered merge; group g = lanes 8g..8g+7 = vertex g, lane = slot
-    const int grp = lane >> 3, slot = lane & 7, gb = grp * 8;
-    const bool gact = act[0] && grp == 0 || act[1] && grp == 1 || act[2] && grp == 2 || act[3] && grp == 3;
-    uint2 e0 = sp[grp][0][slot];
-    int32_t key = (int32_t)e0.x;
-    V val = gact ? (V)e0.y : (V)0;
-    for (int q = 1; q < P; ++q) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint2 e = sp[grp][q][i];
-            const bool live = gact && e.y != 0u;
-            if (!__any_sync(0xffffffffu, live)) continue;
-            const int32_t c = (int32_t)e.x;
-            const V w = (V)e.y;
-            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c, a.zkey)) >> gb) & 0xffu;
-            const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
-            const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
-            const V d = (mm | fm) ? (V)0 : w;
-            if (live) {
-                const bool mine = (sel >> slot) & 1u;
-                if (mine) key = c;
-                val = mine ? val + w : val - (val < d ? val : d);
-            }
-        }
-    }
-    // (C) max_key (sketch.py:93-105) per group
-    bool have = val > (V)0;
-    V bw = have ? val : (V)0;
-    int32_t bk = key;
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-        const V ow = __shfl_xor_sync(0xffffffffu, bw, o);
-        const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
-        if (oh && (!have || ow > bw || (ow == bw && ok < bk))) { bw = ow; bk = ok; have = true; }
-    }
-#pragma unroll
-    for (int j = 0; j < kGrp; ++j) {
-        if (!act[j]) continue;
-        const int32_t best = __shfl_sync(0xffffffffu, bk, j * 8);
-        const int found = __shfl_sync(0xffffffffu, (int)have, j * 8);
-        warp_hi_finish<DET>(a, vv[j], cur[j], found ? best : cur[j], f0[j], lch[j], lo[j], hi[j], lane);
-    }
-}
-
 // High degree, MG, k = 8, R_H <= 32, integer sketch values: lane-parallel
 // merge in two launches.
 //  k_mg_hi_scan: a warp per vertex (lane g = chunk g, register sketch) stores
@@ -1036,7 +765,9 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
     bool lc = false;
     if (a.stream == 1)
         lane_stream_p<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
-            if (valid) part.acc(c, (V)w, 8);
+            if (a.dbg & 2) {  // timing experiment only: the streams without the sketch
+                if (valid) part.s[0] += (uint32_t)c ^ (uint32_t)w;
+            } else if (valid) part.acc(c, (V)w, 8);
         });
     else
         lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
@@ -1341,127 +1072,6 @@ __global__ void __launch_bounds__(kThreads) k_bm_hi_direct(SweepArgs a, const in
     warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
 }
 
-// High degree, MG: warp per vertex, lane g = chunk g of _chunk_bounds(deg,
-// R_H) (lpa.py:178-183) with a register sketch, streamed through the window
-// tile; then parts[1..] are replayed into parts[0] in order (sketch.py:
-// 76-91) on a slot-parallel warp sketch (lane l = slot l).
-template <class W, int K, bool DET, class V>
-__global__ void __launch_bounds__(kWinThreads) k_mg_hi_win(SweepArgs a, const int32_t *__restrict__ list,
-                                                           int64_t count, int round0) {
-    constexpr int S = WinS<W>::S;
-    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
-    __shared__ W s_w[kWinWarps][32][S + 1];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= count) return;  // warp-uniform
-    if (((a.dbg & 4) && wid != 0) || ((a.dbg & 8) && wid == 0)) return;  // timing experiments only
-    const int32_t v = __ldg(&list[wid]);
-    const uint8_t f0 = a.flag_cur[v];
-    if (DET) {
-        if (round0 && !f0) return;
-    } else {
-        if (!f0) return;
-        __syncwarp();
-        if (lane == 0) a.flag_cur[v] = 0;
-    }
-    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-    const int64_t deg = hi - lo;
-    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-    const int k = K > 0 ? K : a.k;
-    const int P = a.parts;
-    bool lower_changed = false;
-    WarpSketch<V> S_{a.zkey, (V)0, a.zkey};
-    for (int b0 = 0; b0 < P; b0 += 32) {
-        const int p = b0 + lane;
-        MgSketchDev<K, V> part;
-        part.reset(k, a.zkey);
-        int64_t cs = 0, ce = 0;
-        if (p < P) chunk_bounds(deg, P, p, cs, ce);
-        window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
-                               [&](int64_t, bool valid, int32_t c, double w) {
-                                         if (valid && !(a.dbg & 2)) part.acc(c, w, k);
-                                     });
-        warp_merge_parts<K, V>(S_, part, b0, P, k, lane);
-    }
-    if (a.scan_double) {  // exact per-key re-count in adjacency order
-        S_.val = (V)0;
-        bool dummy = false;
-        for (int64_t base = lo; base < hi; base += 32) {
-            int64_t x = base + lane;
-            int32_t c = 0;
-            V w = (V)0;
-            bool ok = false;
-            if (x < hi) {
-                int32_t t = __ldg(&a.tgt[x]);
-                if (t != v) {
-                    ok = true;
-                    c = DET ? det_label(a, t, v, dummy) : async_label(a, t);
-                    w = (V)arc_weight<W>(a, x);
-                }
-            }
-            unsigned okm = __ballot_sync(0xffffffffu, ok);
-            while (okm) {
-                int j = __ffs(okm) - 1;
-                okm &= okm - 1;
-                int32_t cj = __shfl_sync(0xffffffffu, c, j);
-                V wj = __shfl_sync(0xffffffffu, w, j);
-                S_.rescan_add(lane, k, cj, wj);
-            }
-        }
-    }
-    int32_t best;
-    const bool found = S_.max_key(lane, k, best);
-    warp_hi_finish<DET>(a, v, cur, found ? best : cur, f0, lower_changed, lo, hi, lane);
-}
-
-// High degree, BM: one vote per chunk, pair-max reduce (lpa.py:143-150).
-template <class W, bool DET, class V>
-__global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const int32_t *__restrict__ list,
-                                                           int64_t count, int round0) {
-    constexpr int S = WinS<W>::S;
-    __shared__ uint32_t s_lab[kWinWarps][32][S + 1];
-    __shared__ W s_w[kWinWarps][32][S + 1];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= count) return;
-    const int32_t v = __ldg(&list[wid]);
-    const uint8_t f0 = a.flag_cur[v];
-    if (DET) {
-        if (round0 && !f0) return;
-    } else {
-        if (!f0) return;
-        __syncwarp();
-        if (lane == 0) a.flag_cur[v] = 0;
-    }
-    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-    const int64_t deg = hi - lo;
-    const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-    const int P = a.parts;
-    bool lower_changed = false;
-    bool have = false;
-    int32_t bc = 0;
-    V bw = (V)0;
-    for (int b0 = 0; b0 < P; b0 += 32) {
-        const int p = b0 + lane;
-        int64_t cs = 0, ce = 0;
-        if (p < P) chunk_bounds(deg, P, p, cs, ce);
-        BmVote<V> st{cur, (V)0};
-        window_streams<W, DET, true>(a, s_lab[wib], s_w[wib], lane, lo + cs, ce - cs, v, lower_changed,
-                               [&](int64_t, bool valid, int32_t c, double w) {
-                                         if (valid) st.acc(c, w);
-                                     });
-        if (p < P && (!have || bm_better(st.w, st.cand, bw, bc))) { bc = st.cand; bw = st.w; have = true; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
-        int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        V ow = __shfl_xor_sync(0xffffffffu, bw, o);
-        if (oh && (!have || bm_better(ow, oc, bw, bc))) { bc = oc; bw = ow; have = true; }
-    }
-    warp_hi_finish<DET>(a, v, cur, bc, f0, lower_changed, lo, hi, lane);
-}
-
 // ================================================================== giant vertices
 // deg >= giant threshold: a single warp per vertex would walk deg/32 arcs per
 // lane with dependent staging latencies on every window -- the tail of every
@@ -1471,7 +1081,7 @@ __global__ void __launch_bounds__(kWinThreads) k_bm_hi_win(SweepArgs a, const in
 //      arcs weight 0 -- coalesced and fully parallel;
 //  (B) scan: a warp per giant, lane g replays chunk g from that contiguous
 //      buffer with register double-buffered prefetch, so the per-lane chain
-//      runs at ALU speed; then the ordered merge as in k_mg_hi_win.
+//      runs at ALU speed; then the ordered merge as in k_mg_hi_direct.
 constexpr int kGatherThreads = 256;
 
 // grid (segments, giants): block x of giant y gathers arcs
@@ -1998,9 +1608,10 @@ int giant_grp_mode() {
     return m;
 }
 
-// Kernel choice per configuration.  Defaults: direct streaming; k = 8 with
-// R_H <= 32 and single scan uses the grouped giant kernel.  The alternatives
-// are kept selectable (SLPA_STAGE, SLPA_HI_GRP, SLPA_GIANT_GRP) so every
+// Kernel choice per configuration.  k = 8 with R_H <= 32 and single scan:
+// scan / lane-parallel merge / finish for the deterministic high-degree
+// rounds and the grouped giant kernel.  SLPA_HI_GRP=0 / SLPA_GIANT_GRP=0
+// select the warp-merge kernels the other configurations use, so every
 // execution path stays covered by the parity matrix (tests/test_gpu_paths.py).
 template <class W, bool DET, class V>
 KernelSet pick_kernels(const slpa_config *cfg) {
@@ -2016,49 +1627,30 @@ KernelSet pick_kernels(const slpa_config *cfg) {
         ks.xmode = 2;
         return ks;
     }
-    const bool direct = stage_mode() != 0;
     if (cfg->variant == SLPA_VARIANT_BM) {
-        if (direct) {
-            KernelSet ks{k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
-                    k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1, 0, nullptr, nullptr, nullptr};
-            ks.lo_small = k_lo_warp<W, DET, V, true>;
-            return ks;
-        }
-        return {k_lane_win<W, BmLane<false, V>, DET>, k_lane_win<W, BmLane<true, V>, DET>, k_bm_hi_win<W, DET, V>,
-                k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kWinThreads, kWinThreads, 1, 0, nullptr, nullptr, nullptr};
+        KernelSet ks{k_lane_direct<W, BmLane<false, V>, DET>, k_lane_direct<W, BmLane<true, V>, DET>,
+                     k_bm_hi_direct<W, DET, V>, k_giant_gather<W, DET>, k_bm_giant<W, DET, V>, kThreads, kThreads, 1,
+                     0, nullptr, nullptr, nullptr};
+        ks.lo_small = k_lo_warp<W, DET, V, true>;
+        return ks;
     }
     if (cfg->sketch_slots != 8) {
-        if (direct) {
-            KernelSet ks{k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
-                    k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads,
-                    kThreads, 1, 0, nullptr, nullptr, nullptr};
-            if (cfg->sketch_slots <= SLPA_KHI_MAX) ks.lo_small = k_lo_warp<W, DET, V, false>;
-            return ks;
-        }
-        return {k_lane_win<W, MgLane<0, false, V>, DET>, k_lane_win<W, MgLane<0, true, V>, DET>,
-                k_mg_hi_win<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kWinThreads,
-                kWinThreads, 1, 0, nullptr, nullptr, nullptr};
+        KernelSet ks{k_lane_direct<W, MgLane<0, false, V>, DET>, k_lane_direct<W, MgLane<0, true, V>, DET>,
+                     k_mg_hi_direct<W, 0, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 0, DET, V>, kThreads,
+                     kThreads, 1, 0, nullptr, nullptr, nullptr};
+        if (cfg->sketch_slots <= SLPA_KHI_MAX) ks.lo_small = k_lo_warp<W, DET, V, false>;
+        return ks;
     }
-    if (!direct)
-        return {k_lane_win<W, MgLane<8, false, V>, DET>, k_lane_win<W, MgLane<8, true, V>, DET>,
-                k_mg_hi_win<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kWinThreads,
-                kWinThreads, 1, 0, nullptr, nullptr, nullptr};
     const bool grouped_ok = cfg->partial_groups <= 32 && cfg->scan_mode != SLPA_SCAN_DOUBLE;
     KernelSet ks{k_lane_direct<W, MgLane<8, false, V>, DET>, k_lane_direct<W, MgLane<8, true, V>, DET>,
                  k_mg_hi_direct<W, 8, DET, V>, k_giant_gather<W, DET>, k_mg_giant<W, 8, DET, V>, kThreads, kThreads,
                  1, 0, nullptr, nullptr, nullptr};
-    if constexpr (sizeof(V) == 4) {
-        if (grouped_ok && hi_grp_mode() == 1) {
-            ks.hi = k_mg_hi_grp<W, DET, V>;
-            ks.hi_threads = kGrpWarps * 32;
-            ks.hi_vpw = kGrp;
-        } else if (grouped_ok && hi_grp_mode() == 2) {
-            if constexpr (DET) {  // async keeps the fused kernel: labels move within the launch
-                ks.hi = k_mg_hi_scan<W, DET, V>;
-                ks.hi_small = k_mg_hi_block<W, DET, V>;
-                ks.hi_merge = k_mg_hi_merge<W, DET, V>;
-                ks.hi_finish = k_mg_hi_finish<DET>;
-            }
+    if constexpr (sizeof(V) == 4 && DET) {  // async keeps the fused kernel: labels move within the launch
+        if (grouped_ok && hi_grp_mode() == 2) {
+            ks.hi = k_mg_hi_scan<W, DET, V>;
+            ks.hi_small = k_mg_hi_block<W, DET, V>;
+            ks.hi_merge = k_mg_hi_merge<W, DET, V>;
+            ks.hi_finish = k_mg_hi_finish<DET>;
         }
     }
     ks.lo_small = k_lo_warp<W, DET, V, false>;

@@ -107,6 +107,7 @@ struct SweepArgs {
     uint32_t *hparts;                 // high degree, lane-parallel merge: part sketches per worklist entry
     uint2 *hmeta;                     //   (cur label, active | f0 << 1 | lower_changed << 2) per entry
     uint32_t *tbits;                  // profiling only (else null): bit v = v's last evaluation took its turn
+    uint32_t *fbits;                  // det commit: next-sweep flag marks (bitmap), then written as bytes
     unsigned char *xs;                // per-unit scratch of the exact / large-k kernels (xmode != 0)
     int64_t xcap;                     //   exact: hash-table slots per warp; large k: unused
     int64_t xunits;                   //   scratch units (threads or warps) the launch may use
@@ -170,6 +171,7 @@ struct WorkBuffers {
     DevBuf<uint32_t> dirty_g, dirty_gp;  // asynchronous giants: their marks / marks waiting for them
     DevBuf<uint8_t> dirty_bytes;  // multi-GPU deterministic: dirty marks exchanged as bytes
     DevBuf<uint32_t> tbits;       // profiling: turn bitmap (the sequential sweep's processed set)
+    DevBuf<uint32_t> fbits;       // det commit: next-sweep flag bitmap
     DevBuf<unsigned long long> dcount;
     DevBuf<int32_t> wl_lo, wl_mid, wl_hi, wl_giant;
     DevBuf<uint32_t> hparts;      // lane-parallel merge scratch (high degree)
@@ -185,7 +187,7 @@ struct WorkBuffers {
     DevBuf<unsigned char> xscratch; // exact / large-k kernels: per-warp hash tables or per-thread sketches
     size_t bytes() const {
         return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() + dirty_g.bytes() + dirty_gp.bytes() +
-               dirty_b.bytes() + tbits.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
+               dirty_b.bytes() + tbits.bytes() + fbits.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes() + xscratch.bytes();
     }
 };

@@ -97,19 +97,6 @@ int giant_async_mode() {
     return m;
 }
 
-// Next-sweep flags: 0 (default) push them from the changed rows; 1 pull them
-// when more than 1 / kPullRatio of the non-isolated vertices changed; 2
-// always pull.  (Measured at RMAT s24: push is faster -- rows without a
-// changed neighbour scan to the end.)
-int commit_mode() {
-    static const int m = [] {
-        const char *e = getenv("SLPA_COMMIT");
-        return e ? atoi(e) : 0;
-    }();
-    return m;
-}
-constexpr int64_t kPullRatio = 4;
-
 // Heavy (deferred) vertices run once the light worklist is at most this size
 // (default: 1/256 of the light vertices, >= 1024; measured at RMAT s24 the
 // light tail rounds then overlap the heavy round instead of preceding it).
@@ -197,6 +184,25 @@ __global__ void __launch_bounds__(kThreads) k_filter_dirty(const int32_t *__rest
     if (hit) out[s_base + s_warp[w] + __popc(m & ((1u << lane) - 1))] = as_index ? (int32_t)i : v;
 }
 
+// Next-sweep flag marks go to a bitmap (n/32 words, L2-resident) with one
+// atomicOr each instead of random byte stores into the n-byte flag array;
+// k_flag_bits_to_bytes then writes the byte flags in one coalesced pass.
+__device__ __forceinline__ void mark_flag(const SweepArgs &a, int32_t t) {
+    atomicOr(&a.fbits[t >> 5], 1u << (t & 31));
+}
+
+__global__ void k_flag_bits_to_bytes(const uint32_t *__restrict__ bits, uint8_t *__restrict__ bytes, int64_t n) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;  // 4 flags per thread
+    if (i >= n) return;
+    const uint32_t w = (__ldg(&bits[i >> 5]) >> (i & 31)) & 0xfu;
+    if (i + 4 <= n) {
+        const uint32_t x = (w & 1u) | ((w & 2u) << 7) | ((w & 4u) << 14) | ((w & 8u) << 21);
+        *reinterpret_cast<uint32_t *>(bytes + i) = x;
+    } else {
+        for (int64_t j = i; j < n; ++j) bytes[j] = (uint8_t)((w >> (j - i)) & 1u);
+    }
+}
+
 // End of a deterministic sweep: fold L1 into L0, count ΔN, and set the
 // next sweep's flags: a changed u marks its out-neighbours t with
 // pos(t) <= pos(u) (those whose turn has passed; lpa.py:223).
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_commit_lo(SweepArgs a, const int32
                 for (int j = 0; j < 8; ++j) t[j] = e0 + j < hi ? __ldg(&a.tgt[e0 + j]) : INT32_MAX;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if (t[j] <= v) a.flag_next[t[j]] = 1;
+                    if (t[j] <= v) mark_flag(a, t[j]);
             }
         }
     }
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_commit_hi(SweepArgs a, const int32
     const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
     for (int64_t e = lo + lane; e < hi; e += 32) {
         int32_t t = __ldg(&a.tgt[e]);
-        if (t <= v) a.flag_next[t] = 1;
+        if (t <= v) mark_flag(a, t);
     }
     __syncwarp();
     if (lane == 0) {
@@ -336,6 +342,7 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     }();
     a.stream = stream;
     a.tbits = ctx->prof_on ? ctx->wb.tbits.p : nullptr;
+    a.fbits = ctx->wb.fbits.p;
     a.zkey = ctx->zkey;
     a.giant_bin = g.bin_giant.p;
     a.giant_off = g.giant_off.p;
@@ -615,73 +622,6 @@ __global__ void __launch_bounds__(kThreads) k_scan_dirty(const uint32_t *__restr
     }
 }
 
-// Pull form of the next-sweep flags (symmetric graphs): F1[t] = some
-// neighbour u >= t changed this sweep (lpa.py:223 marks every neighbour of a
-// changed u; those at or before u are the ones whose turn has passed).  Each
-// row is scanned only until the first such neighbour (rows keep adjacency
-// order, so no suffix shortcut) -- when a large share of the vertices
-// changed this is a few reads per vertex instead of a byte store per arc of
-// every changed row.
-__global__ void __launch_bounds__(kThreads) k_pull_flags_lo(SweepArgs a, const int32_t *__restrict__ list,
-                                                            int64_t count) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    const int32_t t = __ldg(&list[i]);
-    const int64_t hi = __ldg(&a.off[t + 1]);
-    for (int64_t e = __ldg(&a.off[t]); e < hi; e += 4) {
-        int32_t u[4];
-        bool f = false;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) u[j] = e + j < hi ? __ldg(&a.tgt[e + j]) : -1;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) f |= u[j] >= t && (__ldcg(&a.lab_new[u[j]]) >> 31) != 0;
-        if (f) {
-            a.flag_next[t] = 1;
-            return;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_pull_flags_hi(SweepArgs a, const int32_t *__restrict__ list,
-                                                            int64_t count) {
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (wid >= count) return;
-    const int32_t t = __ldg(&list[wid]);
-    const int64_t hi = __ldg(&a.off[t + 1]);
-    for (int64_t e = __ldg(&a.off[t]); e < hi; e += 32) {
-        const int64_t x = e + lane;
-        const int32_t u = x < hi ? __ldg(&a.tgt[x]) : -1;
-        if (__any_sync(0xffffffffu, u >= t && (__ldcg(&a.lab_new[u]) >> 31) != 0)) {
-            if (lane == 0) a.flag_next[t] = 1;
-            return;
-        }
-    }
-}
-
-// Fold L1 into L0 and count the changed vertices (thread per vertex).
-__global__ void __launch_bounds__(kThreads) k_fold_count(SweepArgs a, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long d = 0;
-    if (i < n) {
-        const uint32_t w = a.lab_new[i];
-        if (w & SLPA_CHG) {
-            a.lab_old[i] = (int32_t)(w & SLPA_LMASK);
-            a.lab_new[i] = w & SLPA_LMASK;
-            d = 1;
-        }
-    }
-    warp_count(a.counters, 0, 0, d);
-}
-
-__global__ void __launch_bounds__(kThreads) k_count_changed(const uint32_t *__restrict__ lab_new, int64_t n,
-                                                            unsigned long long *__restrict__ ctr) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool c = i < n && (__ldcg(&lab_new[i]) >> 31) != 0;
-    const unsigned m = __ballot_sync(0xffffffffu, c);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(ctr, (unsigned long long)__popc(m));
-}
-
 // Asynchronous giants: OR a finished batch's dependant marks into the round
 // bitmap and clear them; move a class's round-0 deferral bits to its own set.
 __global__ void k_or_clear(uint32_t *__restrict__ src, uint32_t *__restrict__ dst, int64_t nwords) {
@@ -753,7 +693,7 @@ __global__ void __launch_bounds__(kThreads) k_commit_lo_pos(SweepArgs a, int64_t
                 for (int j = 0; j < 8; ++j) t[j] = e0 + j < hi ? __ldg(&a.tgt[e0 + j]) : INT32_MAX;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if (t[j] <= v) a.flag_next[t[j]] = 1;
+                    if (t[j] <= v) mark_flag(a, t[j]);
             }
         }
     }
@@ -912,14 +852,15 @@ int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg) {
     const int64_t n = g.n;
     const SweepArgs a = make_args(ctx, cfg, 0);
     CUDA_TRY(cudaMemsetAsync(wb.counters.p + CNT_DELTA * CNT_STRIPES, 0, CNT_STRIPES * sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(wb.fbits.p, 0, (size_t)((n + 31) / 32) * sizeof(uint32_t), s));
     if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
     if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
     if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
     if (g.n_giant > 0)
         k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
     if (n > 0) k_fold_all<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, wb.lab_new.p, n);
+    if (n > 0) k_flag_bits_to_bytes<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, s>>>(wb.fbits.p, wb.flag_a.p, n);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(wb.flag_a.p, wb.flag_b.p, (size_t)n, cudaMemcpyDeviceToDevice, s));
     read_counters(ctx);
     ctx->stats.sweeps += 1;
     return (int64_t)ctx->h_sum[CNT_DELTA];
@@ -1124,32 +1065,10 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     giant_join(ctx);
     const unsigned long long evals = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
     const unsigned long long arcs = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
-    // commit: L0 <- L1, delta, next-sweep flags.  Many changed vertices:
-    // pull the flags (a short suffix scan per vertex); few: push them from the
-    // changed rows.
-    bool pull = false;
-    if (g.symmetric && commit_mode() != 0 && n > 0) {
-        wb.dcount.alloc(1);
-        CUDA_TRY(cudaMemsetAsync(wb.dcount.p, 0, sizeof(unsigned long long), s));
-        k_count_changed<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_new.p, n, wb.dcount.p);
-        unsigned long long nchg = 0;
-        CUDA_TRY(cudaMemcpyAsync(&nchg, wb.dcount.p, sizeof(nchg), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        const int64_t active = g.n_lo + g.n_mid + g.n_hi + g.n_giant;
-        pull = commit_mode() == 2 || (int64_t)nchg * kPullRatio > active;
-    }
-    if (pull) {
-        timed_launch(ctx, SLPA_PROF_COMMIT, 5, [&] {
-            if (g.n_lo > 0) k_pull_flags_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
-            const int32_t *heavy[3] = {g.bin_mid.p, g.bin_hi.p, g.bin_giant.p};
-            const int64_t nheavy[3] = {g.n_mid, g.n_hi, g.n_giant};
-            for (int h = 0; h < 3; ++h)
-                if (nheavy[h] > 0)
-                    k_pull_flags_hi<<<grid_for(nheavy[h] * 32, kThreads), kThreads, 0, s>>>(a, heavy[h], nheavy[h]);
-            k_fold_count<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, n);
-            CUDA_TRY(cudaGetLastError());
-        });
-    } else timed_launch(ctx, SLPA_PROF_COMMIT, 4, [&] {
+    // commit: L0 <- L1, delta, next-sweep flags pushed from the changed rows
+    const int64_t fwords = (n + 31) / 32;
+    CUDA_TRY(cudaMemsetAsync(wb.fbits.p, 0, (size_t)fwords * sizeof(uint32_t), s));
+    timed_launch(ctx, SLPA_PROF_COMMIT, 5, [&] {
         if (g.n_lo > 0) {
             if (commit_pos_mode()) k_commit_lo_pos<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, n);
             else k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
@@ -1158,6 +1077,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
         if (g.n_giant > 0)
             k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
+        if (n > 0) k_flag_bits_to_bytes<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, s>>>(wb.fbits.p, wb.flag_b.p, n);
         CUDA_TRY(cudaGetLastError());
     });
     read_counters(ctx);

@@ -51,15 +51,12 @@ ENVS = [
     {"SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
     {"SLPA_HI_SPLIT": "100000"},
     {"SLPA_FORCE_FP64": "1", "SLPA_GIANT": "300"},
-    {"SLPA_HI_GRP": "1", "SLPA_GIANT": "300"},
     {"SLPA_HI_GRP": "0", "SLPA_GIANT": "300"},
     {"SLPA_GIANT_GRP": "0", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "128"},
     {"SLPA_STREAM": "0", "SLPA_GIANT": "5000"},
     {"SLPA_L2_PERSIST_MB": "40"},
     {"SLPA_SCAN": "0", "SLPA_GIANT": "300"},
-    {"SLPA_COMMIT": "0", "SLPA_GIANT": "300"},
-    {"SLPA_COMMIT": "2", "SLPA_GIANT": "300"},
     {"SLPA_DEFER_MIN": "0", "SLPA_GIANT": "300"},
     {"SLPA_DEFER_MIN": "50", "SLPA_GIANT": "300"},
     {"SLPA_GIANT_ASYNC": "0", "SLPA_GIANT": "300"},
@@ -70,8 +67,6 @@ ENVS = [
     {"SLPA_COMMIT_POS": "0", "SLPA_SCAN_SORT_MIN": "0"},
     {"SLPA_LO_SMALL": "100000000", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "1000", "SLPA_HI_SPLIT": "300"},
-    {"SLPA_STAGE": "0", "SLPA_GIANT": "300"},
-    {"SLPA_STAGE": "0", "SLPA_HI_SPLIT": "400", "SLPA_GIANT": "1500"},
 ]
 
 
