@@ -280,8 +280,8 @@ def run_partitioned(args, world, rank, local, dist):
     from paper_2411_19901_b200.distributed import lpa_run_partitioned, partition_ranges
     scale = args.scale + int(round(math.log2(world)))
     n = 1 << scale
-    ranges = partition_ranges(n, world)
     eng = slpa.Engine(local)
+    ranges = eng.rmat_cuts(scale, world, seed=SEED, permute=True)  # arc-balanced contiguous ranges
     eng.part_gen_rmat(scale, *ranges[rank], seed=SEED, permute=True)
     cfg = slpa.LpaConfig(variant=args.variant, worker_count=0 if args.mode == "det" else 1)
     dev = torch.device(f"cuda:{local}")
@@ -322,7 +322,9 @@ def run_partitioned(args, world, rank, local, dist):
                        "mode": ("deterministic (bit-exact sequential; speculative rounds with a per-round "
                                 "label all-gather + dirty-mark max-reduce)") if args.mode == "det"
                                else "async (partitioned)",
-                       "parallelism": f"{world} contiguous vertex ranges, NCCL label all-gather + flag max-reduce",
+                       "parallelism": f"{world} contiguous arc-balanced vertex ranges, NCCL label all-gather + "
+                                      f"flag max-reduce on the library stream",
+                       "ranges": ranges,
                        "l2_policy": "inputs larger than L2"},
             "iterations_per_step": iters_all, "gpu_launches": None, "e2e": None, "roofline": None,
             "cpu_baseline": None, "clocks": clk,

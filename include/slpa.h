@@ -184,6 +184,16 @@ int32_t slpa_part_gen_rmat(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint
                            uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t v_begin,
                            int64_t v_end);
 int32_t slpa_part_info(slpa_ctx *ctx, int64_t *n, int64_t *m_local, int64_t *v_begin, int64_t *v_end);
+/* Arc-balanced contiguous ranges of an RMAT graph over `world` ranks:
+ * cuts[0..world] (cuts[0] = 0, cuts[world] = n), identical on every rank. */
+int32_t slpa_rmat_cuts(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                       uint64_t seed, int32_t permute, uint64_t perm_key, int32_t world, int64_t *cuts);
+/* Symmetry of a partitioned graph: every rank reports the 4 hash sums of its
+ * rows; the caller sums them over the ranks (mod 2^64) and passes
+ * (f1 == r1 && f2 == r2) back.  Deterministic partitioned rounds refuse an
+ * unconfirmed or asymmetric graph (SLPA_EUNSUPPORTED). */
+int32_t slpa_part_arc_hash(slpa_ctx *ctx, uint64_t *hash4);
+int32_t slpa_part_set_symmetric(slpa_ctx *ctx, int32_t symmetric);
 /* Device pointers of the label replica (int32[n]) and flag array (uint8[n]). */
 int32_t slpa_part_buffers(slpa_ctx *ctx, uint64_t *labels_dptr, uint64_t *flags_dptr);
 int32_t slpa_part_begin(slpa_ctx *ctx, const slpa_config *cfg);

@@ -99,6 +99,9 @@ SIGNATURES = {
     "slpa_part_info": (_i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                               ctypes.POINTER(_i64)]),
     "slpa_part_buffers": (_i32, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "slpa_rmat_cuts": (_i32, [_vp, _i32, _i64, _u32, _u32, _u32, _u64, _i32, _u64, _i32, _vp]),
+    "slpa_part_arc_hash": (_i32, [_vp, _vp]),
+    "slpa_part_set_symmetric": (_i32, [_vp, _i32]),
     "slpa_part_begin": (_i32, [_vp, ctypes.POINTER(SlpaConfig)]),
     "slpa_part_sweep": (_i32, [_vp, ctypes.POINTER(SlpaConfig), _i32, ctypes.POINTER(_i64)]),
     "slpa_part_end_exchange": (_i32, [_vp]),

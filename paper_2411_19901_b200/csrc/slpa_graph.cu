@@ -522,6 +522,31 @@ __global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const in
     }
 }
 
+// The four symmetry hash sums of k_arc_checks over the resident rows (a
+// partition's rows: the sums add up across ranks; the graph is symmetric iff
+// the forward and reverse sums agree globally).
+void slpa_arc_hash_impl(slpa_ctx *ctx, uint64_t out[4]) {
+    DeviceGraph &g = ctx->g;
+    cudaStream_t s = ctx->stream;
+    for (int i = 0; i < 4; ++i) out[i] = 0;
+    if (g.n == 0 || g.m == 0) return;
+    DevBuf<unsigned long long> acc;
+    acc.alloc(8);
+    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 8 * sizeof(unsigned long long), s));
+    const unsigned blocks = (unsigned)((g.m + kArcBlock - 1) / kArcBlock);
+    if (g.w_f64)
+        k_arc_checks<double><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const double *)g.w(), g.n, g.m, acc.p,
+                                                      (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
+    else
+        k_arc_checks<float><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const float *)g.w(), g.n, g.m, acc.p,
+                                                     (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i < 4; ++i) out[i] = h[i];
+}
+
 // Symmetry check + reverse CSR of the active numbering; resets the bins.
 void slpa_graph_finalize(slpa_ctx *ctx) {
     DeviceGraph &g = ctx->g;
@@ -1023,6 +1048,71 @@ struct TouchesRange {
     }
 };
 }  // namespace
+
+// Arc-balanced partition of the RMAT graph (multi-GPU): the
+// same counter-based edge stream every rank generates, histogrammed by
+// endpoint (self-loops dropped; duplicates counted, which the cut does not
+// need to resolve), then world-1 cuts where the running arc count crosses
+// r * total / world.  Every rank computes the same cuts.
+__global__ void k_key_degrees(const uint64_t *__restrict__ keys, int64_t cnt, uint64_t drop,
+                              unsigned long long *__restrict__ deg) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    const uint64_t k = keys[i];
+    if (k == drop) return;
+    atomicAdd(&deg[k >> 32], 1ull);
+    atomicAdd(&deg[k & 0xFFFFFFFFULL], 1ull);
+}
+__global__ void k_find_cuts(const unsigned long long *__restrict__ incl, int64_t n, int32_t world,
+                            int64_t *__restrict__ cuts) {
+    const int r = threadIdx.x + 1;  // cuts[1..world-1]
+    if (r >= world) return;
+    const unsigned long long total = incl[n - 1];
+    const unsigned long long want = (unsigned long long)((double)total * r / world);
+    int64_t lo = 0, hi = n;  // first v with incl[v] > want ... vertices [0, v] hold <= want + deg
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (incl[mid] <= want) lo = mid + 1;
+        else hi = mid;
+    }
+    cuts[r] = lo;
+}
+
+void slpa_rmat_cuts_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                         uint64_t seed, int32_t permute, uint64_t perm_key, int32_t world, int64_t *cuts_out) {
+    SLPA_REQUIRE(scale >= 1 && scale <= 31, SLPA_EINVAL, "rmat scale must be in [1, 31]");
+    SLPA_REQUIRE(world >= 1 && world <= 1024, SLPA_EINVAL, "world must be in [1, 1024]");
+    const int64_t n = 1LL << scale;
+    cudaStream_t s = ctx->stream;
+    const int64_t chunk = std::min<int64_t>(std::max<int64_t>(num_edges, 1), 1LL << 27);
+    DevBuf<uint64_t> buf;
+    DevBuf<unsigned long long> deg, incl;
+    DevBuf<int64_t> cuts;
+    buf.alloc(chunk);
+    deg.alloc(n);
+    incl.alloc(n);
+    cuts.alloc(world + 1);
+    CUDA_TRY(cudaMemsetAsync(deg.p, 0, (size_t)n * sizeof(unsigned long long), s));
+    for (int64_t e0 = 0; e0 < num_edges; e0 += chunk) {
+        const int64_t cnt = std::min(chunk, num_edges - e0);
+        k_gen_rmat<<<grid_for(cnt, kT), kT, 0, s>>>(scale, e0, cnt, tA, tAB, tABC, seed, permute, perm_key,
+                                                    drop_key(n), buf.p);
+        k_key_degrees<<<grid_for(cnt, kT), kT, 0, s>>>(buf.p, cnt, drop_key(n), deg.p);
+        CUDA_TRY(cudaGetLastError());
+    }
+    unsigned long long *in = deg.p, *out = incl.p;
+    const int64_t nn = n;
+    cub_call(ctx, [&](void *tmp, size_t &bytes) { return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, nn, s); });
+    std::vector<int64_t> h((size_t)world + 1, 0);
+    h[world] = n;
+    CUDA_TRY(cudaMemcpyAsync(cuts.p, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (world > 1) k_find_cuts<<<1, 1024, 0, s>>>(incl.p, n, world, cuts.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(h.data(), cuts.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int r = 1; r <= world; ++r) h[r] = std::max(h[r], h[r - 1]);  // monotone
+    std::copy(h.begin(), h.end(), cuts_out);
+}
 
 // One rank's rows of the RMAT graph: every rank generates the
 // same edge stream (counter-based RNG) in chunks, keeps the pairs touching

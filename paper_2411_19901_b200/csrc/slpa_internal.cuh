@@ -223,6 +223,7 @@ struct slpa_ctx {
     size_t l2_prev_limit = 0;  //   ... which was this before
     // multi-GPU partition
     int32_t part = 0;
+    int32_t part_sym_known = 0;  // the ranks' combined arc hashes confirmed g.symmetric
     int64_t v_begin = 0, v_end = 0;
 };
 

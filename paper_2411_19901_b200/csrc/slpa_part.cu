@@ -20,6 +20,9 @@ void slpa_part_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, ui
                              uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t r0,
                              int64_t r1);
 void slpa_part_tally_impl(slpa_ctx *ctx, double *internal_local, uint64_t *incident_dptr, uint64_t *sizes_dptr);
+void slpa_arc_hash_impl(slpa_ctx *ctx, uint64_t out[4]);
+void slpa_rmat_cuts_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                         uint64_t seed, int32_t permute, uint64_t perm_key, int32_t world, int64_t *cuts_out);
 void slpa_part_modularity_impl(slpa_ctx *ctx, double internal_total, double *q);
 
 namespace {
@@ -57,7 +60,12 @@ void mark_partitioned(slpa_ctx *ctx, int64_t vb, int64_t ve) {
     g.has_order = 0;
     g.roff.release();
     g.rsrc.release();
-    g.symmetric = 1;  // only the asynchronous sweep runs partitioned
+    // Symmetry is a property of the whole graph: unknown until the ranks
+    // combine their arc hashes (slpa_part_arc_hash -> slpa_part_set_symmetric).
+    // The asynchronous sweep does not depend on it; the deterministic rounds
+    // require it (their dependant marks follow out-arcs).
+    g.symmetric = 0;
+    ctx->part_sym_known = 0;
     slpa_check_int_weights(ctx);
     g.max_deg = -1;
     g.bin_thr = -1;
@@ -116,6 +124,30 @@ int32_t slpa_part_gen_rmat(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint
     return guard(ctx, [&] {
         slpa_part_gen_rmat_impl(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key, v_begin, v_end);
         mark_partitioned(ctx, v_begin, v_end);
+    });
+}
+
+int32_t slpa_rmat_cuts(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
+                       uint64_t seed, int32_t permute, uint64_t perm_key, int32_t world, int64_t *cuts) {
+    return guard(ctx, [&] {
+        SLPA_REQUIRE(cuts != nullptr, SLPA_EINVAL, "cuts is NULL");
+        slpa_rmat_cuts_impl(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key, world, cuts);
+    });
+}
+
+int32_t slpa_part_arc_hash(slpa_ctx *ctx, uint64_t *hash4) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        SLPA_REQUIRE(hash4 != nullptr, SLPA_EINVAL, "hash4 is NULL");
+        slpa_arc_hash_impl(ctx, hash4);
+    });
+}
+
+int32_t slpa_part_set_symmetric(slpa_ctx *ctx, int32_t symmetric) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        ctx->g.symmetric = symmetric ? 1 : 0;
+        ctx->part_sym_known = 1;
     });
 }
 
@@ -185,6 +217,9 @@ int32_t slpa_part_det_round(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickl
         slpa_validate_config(cfg);
         require_part(ctx);
         SLPA_REQUIRE(cfg->worker_count == 0, SLPA_EINVAL, "deterministic rounds need worker_count == 0");
+        SLPA_REQUIRE(ctx->part_sym_known && ctx->g.symmetric, SLPA_EUNSUPPORTED,
+                     "partitioned deterministic sweeps need a symmetric graph (confirmed with "
+                     "slpa_part_arc_hash / slpa_part_set_symmetric)");
         SLPA_REQUIRE(ctx->wb.dirty_bytes.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
         slpa_ensure_bins(ctx, cfg);
         slpa_part_det_round_impl(ctx, cfg, pickless ? 1 : 0, round);

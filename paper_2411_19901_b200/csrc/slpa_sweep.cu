@@ -822,7 +822,7 @@ void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickles
     giant_join(ctx);
     if (n > 0) k_dirty_bits_to_bytes<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, wb.dirty_bytes.p, n);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaStreamSynchronize(s));
+    // no host sync: the caller's exchange is queued on ctx->stream behind these kernels
     ctx->stats.rounds += 1;
 }
 

@@ -107,17 +107,60 @@ def _sync(t):
         torch.cuda.current_stream(t.device).synchronize()
 
 
+class _OnLibraryStream:
+    """Run torch work (the collectives and their staging copies) on the
+    library's own CUDA stream: the exchange is ordered after the sweep's
+    kernels and before the next library call on the device, with no host
+    synchronisation in between (NCCL's internal stream joins the current
+    stream through events)."""
+
+    def __init__(self, engine, device):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.ext = torch.cuda.ExternalStream(engine.stream(), device=device) if device.type == "cuda" else None
+        self.ctx = None
+
+    def __enter__(self):
+        if self.ext is not None:
+            self.ctx = self.torch.cuda.stream(self.ext)
+            self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+        return False
+
+
+def confirm_symmetric(engine, group=None) -> bool:
+    """Combine the ranks' arc hashes: the partitioned graph is
+    symmetric iff the global forward and reverse sums agree; the library is
+    told the answer (its deterministic rounds require a symmetric graph)."""
+    import torch
+    import torch.distributed as dist
+    h = engine.part_arc_hash().view(np.int64)  # two's complement: sums wrap mod 2^64 on every backend
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.tensor(h.copy(), dtype=torch.int64, device=dev)
+    dist.all_reduce(t, group=group)
+    v = t.cpu().numpy()
+    sym = bool(v[0] == v[1] and v[2] == v[3])
+    engine.part_set_symmetric(sym)
+    return sym
+
+
 def _det_sweep(engine, cfg, pickless, ex, lab_new, dirty) -> int:
     """One deterministic partitioned sweep: speculative rounds until no rank
     holds a dirty vertex, then the commit.  Returns the
     rank-local count of changed owned vertices."""
     rnd = 0
+    on_lib = _OnLibraryStream(engine, lab_new.device)
     while True:
-        engine.part_det_round(cfg, pickless, rnd)  # returns after its stream drained
-        ex.labels(lab_new)
-        ex.flags(dirty)
-        _sync(lab_new)
-        if engine.part_det_import() == 0:  # global count: identical on every rank
+        engine.part_det_round(cfg, pickless, rnd)  # kernels queued on the library stream
+        with on_lib:  # the exchange follows them on the same stream
+            ex.labels(lab_new)
+            ex.flags(dirty)
+        if engine.part_det_import() == 0:  # global count (identical on every rank): the round's one sync
             break
         rnd += 1
     return engine.part_det_commit(cfg)
@@ -131,9 +174,13 @@ def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) ->
     cfg.validate()
     ex = Exchange(ranges, group)
     n = engine.n
+    det = cfg.worker_count == 0
+    if det and not confirm_symmetric(engine, group):
+        raise ValueError("the partitioned deterministic sweep needs a symmetric graph "
+                         "(every arc's reverse present with the same weight); use worker_count > 0")
     engine.part_begin(cfg)
     lab, fl = engine.part_buffers()
-    det = cfg.worker_count == 0
+    on_lib = _OnLibraryStream(engine, lab.device)
     if det:
         lab_new, dirty = engine.part_det_buffers()
     history = []
@@ -143,11 +190,12 @@ def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) ->
         if det:
             local = _det_sweep(engine, cfg, pickless, ex, lab_new, dirty)
         else:
-            local = engine.part_sweep(cfg, pickless)  # returns after its stream drained
-            ex.labels(lab)
-        ex.flags(fl)
-        _sync(lab)  # collectives on torch's stream finish before the library touches the buffers
-        engine.part_end_exchange()
+            local = engine.part_sweep(cfg, pickless)
+        with on_lib:
+            if not det:
+                ex.labels(lab)
+            ex.flags(fl)
+        engine.part_end_exchange()  # library stream: after the exchange
         delta = ex.sum(local, lab.device)
         history.append(delta)
         if iteration_hook is not None:

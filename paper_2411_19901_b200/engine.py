@@ -272,6 +272,25 @@ class Engine:
         check(self.lib, self.ctx, rc)
         return self._part_refresh()
 
+    def rmat_cuts(self, scale, world, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, permute=True, perm_key=7):
+        """Arc-balanced contiguous ranges [(begin, end)] of the RMAT graph over
+        `world` ranks (the same on every rank; computed on this device)."""
+        ta, tab, tabc = rmat_thresholds(a, b, c)
+        cuts = np.zeros(int(world) + 1, dtype=np.int64)
+        rc = self.lib.slpa_rmat_cuts(self.ctx, int(scale), int(edge_factor) << int(scale), ta, tab, tabc, int(seed),
+                                     1 if permute else 0, int(perm_key), int(world), cuts.ctypes.data)
+        check(self.lib, self.ctx, rc)
+        return [(int(cuts[r]), int(cuts[r + 1])) for r in range(int(world))]
+
+    def part_arc_hash(self):
+        """The 4 symmetry hash sums of this rank's rows (uint64, add up over ranks)."""
+        h = np.zeros(4, dtype=np.uint64)
+        check(self.lib, self.ctx, self.lib.slpa_part_arc_hash(self.ctx, h.ctypes.data))
+        return h
+
+    def part_set_symmetric(self, symmetric: bool):
+        check(self.lib, self.ctx, self.lib.slpa_part_set_symmetric(self.ctx, 1 if symmetric else 0))
+
     def part_upload(self, n, v_begin, v_end, row_offsets, targets, weights):
         """Rows [v_begin, v_end): row_offsets int64[v_end-v_begin+1] (from 0),
         targets int32 (global ids), weights float32|float64."""

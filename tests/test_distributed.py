@@ -203,6 +203,21 @@ class MockDetEngine(MockEngine):
     def part_det_buffers(self):
         return self.lab_new, self.dirty
 
+    def part_arc_hash(self):
+        """Additive forward / reverse arc sums of the owned rows (the
+        library's k_arc_checks hashes, restated with a simpler mix)."""
+        g = self.g
+        mask = np.uint64((1 << 64) - 1)
+        f = r = np.uint64(0)
+        for v in range(self.v_begin, self.v_end):
+            for t in g.targets[g.offsets[v]:g.offsets[v + 1]]:
+                f = (f + np.uint64((v * 1000003 + int(t)) * 2654435761 % (1 << 61))) & mask
+                r = (r + np.uint64((int(t) * 1000003 + v) * 2654435761 % (1 << 61))) & mask
+        return np.array([f, r, f, r], dtype=np.uint64)
+
+    def part_set_symmetric(self, symmetric):
+        self.symmetric = symmetric
+
     def part_det_round(self, cfg, pickless, rnd):
         g = self.g
         L0 = self.lab.numpy()
@@ -296,9 +311,8 @@ def _gpu_det_worker(rank, world, port, scale, variant, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    n = 1 << scale
-    ranges = partition_ranges(n, world)
     eng = slpa.Engine(0)
+    ranges = eng.rmat_cuts(scale, world, seed=78, permute=True)  # arc-balanced
     eng.part_gen_rmat(scale, *ranges[rank], seed=78, permute=True)
     cfg = slpa.LpaConfig(variant=variant)
     res = lpa_run_partitioned(eng, cfg, ranges)
@@ -346,3 +360,68 @@ def test_bench_multi_rank_path(mode):
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["vertices"] == 1 << 16
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_rmat_cuts_arc_balanced(oracle, world):
+    """Engine.rmat_cuts: the device histogram of the RMAT edge stream gives the
+    same cuts as numpy on the oracle's edge stream (multigraph degrees), and
+    the ranges cover [0, n) with near-equal arc counts of the merged CSR."""
+    import paper_2411_19901_b200 as slpa
+    from oracle.oracle import rmat_thresholds
+    scale = 14
+    eng = slpa.Engine(0)
+    ranges = eng.rmat_cuts(scale, world, seed=5, permute=True)
+    n = 1 << scale
+    ne = 16 << scale
+    src = np.empty(ne, dtype=np.uint32)
+    dst = np.empty(ne, dtype=np.uint32)
+    ta, tab, tabc = rmat_thresholds(0.57, 0.19, 0.19)
+    k = oracle.lib.orc_rmat_edges(scale, ne, ta, tab, tabc, 5, 1, 7, src.ctypes.data, dst.ctypes.data)
+    deg = np.bincount(np.concatenate([src[:k], dst[:k]]).astype(np.int64), minlength=n)
+    incl = np.cumsum(deg)
+    want = [0] + [int(np.searchsorted(incl, int(incl[-1] * r / world), side="right")) for r in range(1, world)] + [n]
+    want = np.maximum.accumulate(want)
+    assert ranges == [(int(want[r]), int(want[r + 1])) for r in range(world)]
+    g = oracle.rmat(scale, seed=5, permute=True)
+    arcs = [int(g.offsets[e] - g.offsets[b]) for b, e in ranges]
+    assert max(arcs) <= 1.05 * g.num_arcs / world
+
+
+def _asym_worker(rank, world, port, out):
+    import torch.distributed as dist
+    import paper_2411_19901_b200 as slpa
+    from paper_2411_19901_b200.distributed import lpa_run_partitioned
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 8
+    ranges = [(0, 4), (4, 8)]
+    b, e = ranges[rank]
+    # a directed ring: every arc's reverse is missing
+    ro = np.arange(e - b + 1, dtype=np.int64)
+    tg = np.array([(v + 1) % n for v in range(b, e)], dtype=np.int32)
+    eng = slpa.Engine(0)
+    eng.part_upload(n, b, e, ro, tg, np.ones(e - b, dtype=np.float32))
+    try:
+        lpa_run_partitioned(eng, slpa.LpaConfig(), ranges)
+        out[rank] = "ran"
+    except ValueError as ex:
+        out[rank] = "ValueError: " + str(ex)
+    res = lpa_run_partitioned(eng, slpa.LpaConfig(worker_count=1), ranges)  # the async sweep accepts it
+    out[rank] = out[rank] + f" | async {res.iterations}"
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_partitioned_det_rejects_asymmetric():
+    """ADVICE r1: the deterministic partitioned rounds need a symmetric graph;
+    the ranks' combined arc hashes detect a directed one and the run refuses
+    (the asynchronous sweep does not depend on symmetry)."""
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_asym_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        assert out[r].startswith("ValueError") and "symmetric" in out[r] and "| async" in out[r]
