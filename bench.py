@@ -253,13 +253,15 @@ def workload_config(args, n, m, world):
     if getattr(args, "graph", "rmat") != "rmat":
         name = {"grid": "4899x4899 4-neighbour grid, unit weights, permuted ids (configs[2])",
                 "kmer": "k-mer-like chain graph, 2e8 vertices, links kept w.p. 0.95 + n/20 chords, permuted ids (configs[3])"}
-        return {"workload": f"nu{'MG8' if args.variant == 'mg' else 'BM'}-LPA {args.graph} ({name[args.graph]})",
+        vname = {"mg": "MG8", "bm": "BM", "exact": "exact"}[args.variant]
+        return {"workload": f"nu{vname}-LPA {args.graph} ({name[args.graph]})",
                 "graph": name[args.graph], "vertices": n, "arcs": m, "variant": args.variant,
                 "mode": "deterministic (bit-exact sequential)" if args.mode == "det" else "async",
                 "parallelism": "single GPU", "l2_policy": "inputs larger than L2"}
     return {
-        "workload": f"nuMG8-LPA RMAT s{args.scale} ef16 (configs[1])" if args.variant == "mg"
-        else f"nuBM-LPA RMAT s{args.scale} ef16",
+        "workload": (f"nuMG8-LPA RMAT s{args.scale} ef16 " + ("(configs[1])" if args.scale == 24 else
+                     "(configs[4]'s graph on one GPU)" if args.scale == 27 else "")).strip() if args.variant == "mg"
+        else f"nu{'BM' if args.variant == 'bm' else 'exact'}-LPA RMAT s{args.scale} ef16",
         "graph": f"RMAT scale {args.scale}, edge factor 16, A/B/C/D .57/.19/.19/.05, permuted ids, "
                  f"self-loops dropped, duplicates merged (seed {SEED})",
         "vertices": n, "arcs": m, "variant": args.variant,
@@ -343,7 +345,7 @@ def main():
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--graph", default="rmat", choices=["rmat", "grid", "kmer"],
                     help="rmat: configs[1] (default); grid: configs[2] 4899^2 grid; kmer: configs[3] 2e8-vertex k-mer-like")
-    ap.add_argument("--variant", default="mg", choices=["mg", "bm"])
+    ap.add_argument("--variant", default="mg", choices=["mg", "bm", "exact"])
     ap.add_argument("--mode", default="det", choices=["det", "async"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--ref-budget", type=float, default=60.0,
@@ -351,6 +353,7 @@ def main():
     ap.add_argument("--py-seconds", type=float, default=10.0,
                     help="Python reference sample (baseline/_ref) beside the CPU numbers; 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (graphs beyond host RAM)")
     args = ap.parse_args()
     world, rank, local = dist_env()
 
@@ -451,7 +454,7 @@ def main():
     e2e = None
     host_graph = None
     int_path = False
-    if rank == 0 or world > 1:
+    if (rank == 0 or world > 1) and not args.no_e2e:
         off, tgt, w = eng.download()
         # the device's exactness test for integer sketch values (slpa_graph.cu)
         nz = np.diff(off) > 0  # reduceat needs in-range starts: non-empty rows only

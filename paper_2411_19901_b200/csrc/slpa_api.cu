@@ -107,9 +107,9 @@ void slpa_alloc_work(slpa_ctx *ctx) {
         wb.dirty_g.alloc(n / 32 + 1);
         wb.dirty_gp.alloc(n / 32 + 1);
     }
-    wb.wl_lo.alloc(n);
-    wb.wl_mid.alloc(n);
-    wb.wl_hi.alloc(n);
+    wb.wl_lo.alloc(n);  // (bins are filled before the work buffers: the worklists are sized by class)
+    wb.wl_mid.alloc(ctx->g.n_mid + 1);
+    wb.wl_hi.alloc(ctx->g.n_hi + 1);
     wb.wl_giant.alloc(ctx->g.n_giant + 1);
     wb.glab.alloc(ctx->g.giant_arcs + 1);
     wb.gw.alloc((ctx->g.giant_arcs + 1) * (ctx->g.w_f64 ? sizeof(double) : sizeof(float)));

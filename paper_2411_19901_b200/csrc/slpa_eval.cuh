@@ -1389,11 +1389,12 @@ __global__ void __launch_bounds__(kThreads) k_exact_warp(SweepArgs a, const int3
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = a.xunits;
     if (gw >= nw) return;
-    const int64_t cap = a.xcap;  // power of two
-    int32_t *keys = reinterpret_cast<int32_t *>(a.xs) + (size_t)gw * (size_t)cap;
-    double *tot = reinterpret_cast<double *>(a.xs + (size_t)a.xunits * (size_t)cap * 4) + (size_t)gw * (size_t)cap;
+    int32_t *keys = reinterpret_cast<int32_t *>(a.xs) + (size_t)gw * (size_t)a.xcap;  // this warp's region
+    double *tot = a.xtot + (size_t)gw * (size_t)a.xcap;
     for (int64_t idx = gw; idx < count; idx += nw) {
         const int32_t v = __ldg(&list[idx]);
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        if (hi - lo <= a.xdeg_lo || hi - lo > a.xdeg_hi) continue;  // the other launch's degree tier
         const uint8_t f0 = a.flag_cur[v];
         const bool go = DET ? (!round0 || f0) : (f0 != 0);
         if (!go) continue;  // warp-uniform
@@ -1401,7 +1402,8 @@ __global__ void __launch_bounds__(kThreads) k_exact_warp(SweepArgs a, const int3
             __syncwarp();
             if (lane == 0) a.flag_cur[v] = 0;
         }
-        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+        int64_t cap = 64;  // this vertex's table: >= 2 x degree slots, so scans and clears stay O(deg)
+        while (cap < 2 * (hi - lo)) cap <<= 1;
         const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
         bool lower_changed = false;
         for (int64_t e0 = lo; e0 < hi; e0 += 32) {

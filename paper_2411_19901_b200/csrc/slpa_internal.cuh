@@ -111,6 +111,8 @@ struct SweepArgs {
     unsigned char *xs;                // per-unit scratch of the exact / large-k kernels (xmode != 0)
     int64_t xcap;                     //   exact: hash-table slots per warp; large k: unused
     int64_t xunits;                   //   scratch units (threads or warps) the launch may use
+    double *xtot;                     //   exact: the tables' binary64 totals (keys in xs)
+    int64_t xdeg_lo, xdeg_hi;         //   exact: this launch takes the vertices with xdeg_lo < degree <= xdeg_hi
     int32_t zkey;                     // internal value of label 0 (0 unless caller labels were remapped)
 };
 
@@ -184,11 +186,12 @@ struct WorkBuffers {
     DevBuf<double> metric_d;    // tallies for modularity
     DevBuf<unsigned long long> metric_u;
     DevBuf<unsigned char> scratch;  // cub temp storage
-    DevBuf<unsigned char> xscratch; // exact / large-k kernels: per-warp hash tables or per-thread sketches
+    DevBuf<unsigned char> xscratch; // exact / large-k kernels: per-warp hash-table keys or per-thread sketches
+    DevBuf<double> xtotals;         // exact: per-warp hash-table totals
     size_t bytes() const {
         return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() + dirty_g.bytes() + dirty_gp.bytes() +
                dirty_b.bytes() + tbits.bytes() + fbits.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
-               counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes() + xscratch.bytes();
+               counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes() + xscratch.bytes() + xtotals.bytes();
     }
 };
 

@@ -310,6 +310,8 @@ KernelSet kernels_for(const slpa_ctx *ctx, const slpa_config *cfg, bool det) {
 
 SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     ctx->cur_cfg = cfg;
+    ctx->wb.wl_mid.alloc(ctx->g.n_mid + 1);  // worklists sized by the current bins (no-op when large enough)
+    ctx->wb.wl_hi.alloc(ctx->g.n_hi + 1);
     SweepArgs a{};
     DeviceGraph &g = ctx->g;
     a.off = g.off();
@@ -431,41 +433,40 @@ int64_t graph_max_degree(slpa_ctx *ctx) {
     return g.max_deg;
 }
 
-// Scratch of the exact (xmode 1: an open-addressing table of xcap slots per
-// warp -- keys, then binary64 totals) and large-k (xmode 2: two k-slot
-// sketches per thread) kernels.  A fixed number of units (warps / threads,
-// at most ~1 GiB) stride over the worklist, so the layout only changes with
-// the table size or k; the exact tables start empty (key -1, total 0.0) and
-// the kernel leaves them so.
-void setup_xscratch(slpa_ctx *ctx, const KernelSet &ks, const slpa_config *cfg, SweepArgs &a) {
+// Scratch of the exact (xmode 1) and large-k (xmode 2) kernels.
+//  exact: open-addressing tables (int32 keys, binary64 totals) of 2^26 slots
+//    in all, kept empty (key -1, total 0.0; the kernel clears the slots it
+//    used).  Two launches: vertices of degree <= 4096 with 8192-slot regions
+//    per warp (thousands of warps), larger ones with regions sized for the
+//    largest degree (a few warps);
+//  large k: two k-slot sketches per thread, a fixed number of threads (at
+//    most ~1 GiB) striding over the worklist.
+constexpr int64_t kExactSmallDeg = 4096;
+
+void setup_xscratch_bigk(slpa_ctx *ctx, const slpa_config *cfg, SweepArgs &a) {
     const size_t budget = (size_t)1 << 30;
-    int64_t cap = 0;
-    size_t per_unit;
-    if (ks.xmode == 1) {
-        cap = 64;
-        while (cap < 2 * std::max<int64_t>(graph_max_degree(ctx), 1)) cap <<= 1;
-        per_unit = (size_t)cap * 12;
-    } else {
-        const size_t vb = ctx->g.int_weights ? 4 : 8;
-        per_unit = (size_t)cfg->sketch_slots * 2 * (4 + vb);
-    }
+    const size_t vb = ctx->g.int_weights ? 4 : 8;
+    const size_t per_unit = (size_t)cfg->sketch_slots * 2 * (4 + vb);
     int64_t units = std::min<int64_t>((int64_t)ctx->num_sms * 64, (int64_t)(budget / per_unit));
     units = std::max<int64_t>(32, units / 32 * 32);
-    const int64_t key = ks.xmode == 1 ? cap : -cfg->sketch_slots;
     const size_t need = per_unit * (size_t)units;
-    if (ctx->xs_key != key || ctx->xs_units != units || ctx->wb.xscratch.count < need) {
-        ctx->wb.xscratch.alloc(need);
-        if (ks.xmode == 1) {
-            CUDA_TRY(cudaMemsetAsync(ctx->wb.xscratch.p, 0xff, (size_t)units * cap * 4, ctx->stream));
-            CUDA_TRY(cudaMemsetAsync(ctx->wb.xscratch.p + (size_t)units * cap * 4, 0, (size_t)units * cap * 8,
-                                     ctx->stream));
-        }
-        ctx->xs_key = key;
-        ctx->xs_units = units;
-    }
+    if (ctx->wb.xscratch.count < need) ctx->wb.xscratch.alloc(need);
+    ctx->xs_key = 0;  // the exact tables' contents are gone
     a.xs = ctx->wb.xscratch.p;
-    a.xcap = cap;
     a.xunits = units;
+}
+
+void setup_xscratch_exact(slpa_ctx *ctx) {
+    int64_t cap_big = 64;
+    while (cap_big < 2 * std::max<int64_t>(graph_max_degree(ctx), 1)) cap_big <<= 1;
+    const int64_t slots = std::max<int64_t>((int64_t)1 << 26, cap_big);
+    if (ctx->xs_key != slots) {
+        ctx->wb.xscratch.alloc((size_t)slots * 4);
+        ctx->wb.xtotals.alloc((size_t)slots);
+        CUDA_TRY(cudaMemsetAsync(ctx->wb.xscratch.p, 0xff, (size_t)slots * 4, ctx->stream));
+        CUDA_TRY(cudaMemsetAsync(ctx->wb.xtotals.p, 0, (size_t)slots * 8, ctx->stream));
+        ctx->xs_key = slots;
+    }
 }
 
 void launch_lane(slpa_ctx *ctx, const KernelSet &ks, int which, const SweepArgs &a0, const int32_t *list, int64_t cnt,
@@ -473,14 +474,40 @@ void launch_lane(slpa_ctx *ctx, const KernelSet &ks, int which, const SweepArgs 
     if (cnt <= 0) return;
     const EvalKernel k = which == 0 ? ks.lo : ks.mid;
     const int threads = ks.lo_threads;
-    if (ks.xmode) {
+    if (ks.xmode == 2) {
         SweepArgs a = a0;
-        setup_xscratch(ctx, ks, ctx->cur_cfg, a);
-        const int64_t items = ks.xmode == 1 ? a.xunits * 32 : a.xunits;
+        setup_xscratch_bigk(ctx, ctx->cur_cfg, a);
         timed_launch(ctx, cls, 1, [&] {
-            k<<<grid_for(items, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
+            k<<<grid_for(a.xunits, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
             CUDA_TRY(cudaGetLastError());
         });
+        return;
+    }
+    if (ks.xmode == 1) {
+        setup_xscratch_exact(ctx);
+        const int64_t slots = ctx->xs_key, maxdeg = graph_max_degree(ctx);
+        for (int tier = 0; tier < 2; ++tier) {
+            SweepArgs a = a0;
+            int64_t cap = 64;
+            if (tier == 0) {
+                cap = 2 * kExactSmallDeg;
+                a.xdeg_lo = -1;
+                a.xdeg_hi = kExactSmallDeg;
+            } else {
+                if (maxdeg <= kExactSmallDeg) break;
+                while (cap < 2 * maxdeg) cap <<= 1;
+                a.xdeg_lo = kExactSmallDeg;
+                a.xdeg_hi = INT64_MAX;
+            }
+            a.xs = ctx->wb.xscratch.p;
+            a.xtot = ctx->wb.xtotals.p;
+            a.xcap = cap;
+            a.xunits = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * 64, slots / cap));
+            timed_launch(ctx, cls, 1, [&] {
+                k<<<grid_for(a.xunits * 32, threads), threads, 0, ctx->stream>>>(a, list, cnt, round0);
+                CUDA_TRY(cudaGetLastError());
+            });
+        }
         return;
     }
     const EvalKernel small = (allow_small && which == 0) ? ks.lo_small : nullptr;
@@ -497,32 +524,51 @@ void launch_lane(slpa_ctx *ctx, const KernelSet &ks, int which, const SweepArgs 
     });
 }
 
+// High-degree rounds.  The scan / merge / finish split stages 2 KB of part
+// sketches per vertex; large rounds run in slices of kHiSlice vertices so the
+// scratch stays at kHiSlice x 2 KB (128 MB) instead of scaling with the bin
+// (1.1 GB at RMAT s24).  Any evaluation order within a round reaches the same
+// fixpoint; a later slice simply sees an earlier one's labels.
+constexpr int64_t kHiSlice = 65536;
+
 void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
                int cls) {
     if (cnt <= 0) return;
     SweepArgs aa = a;
-    if (ks.hi_merge) {  // scratch for the lane-parallel merge (sized for the whole high-degree bin)
+    const bool small = ks.hi_small && cnt <= hi_small_max();
+    if (ks.hi_merge && !small) {
         WorkBuffers &wb = ctx->wb;
-        const int64_t cap = ctx->g.n_hi;
+        const int64_t cap = std::min<int64_t>(std::max<int64_t>(ctx->g.n_hi, 1), kHiSlice);
         wb.hparts.alloc((size_t)cap * kLpmWords);
         wb.hmeta.alloc((size_t)cap);
         aa.hparts = wb.hparts.p;
         aa.hmeta = wb.hmeta.p;
     }
-    timed_launch(ctx, cls, ks.hi_merge ? 3 : 1, [&] {
-        const int64_t items = ks.hi_vpw ? (cnt + ks.hi_vpw - 1) / ks.hi_vpw * 32 : cnt;
-        if (ks.hi_small && cnt <= hi_small_max()) {  // fused block-per-vertex kernel (merge + finish inside)
+    if (small) {  // fused block-per-vertex kernel (merge + finish inside)
+        timed_launch(ctx, cls, 1, [&] {
             ks.hi_small<<<(unsigned)cnt, kGiantWarps * 32, 0, ctx->stream>>>(aa, list, cnt, round0);
             CUDA_TRY(cudaGetLastError());
-            return;
-        }
-        ks.hi<<<grid_for(items, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(aa, list, cnt, round0);
-        if (ks.hi_merge) {
-            ks.hi_merge<<<grid_for(cnt, kThreads), kThreads, 0, ctx->stream>>>(aa, list, cnt, round0);
-            ks.hi_finish<<<grid_for(cnt * 32, kThreads), kThreads, 0, ctx->stream>>>(aa, list, cnt, round0);
-        }
-        CUDA_TRY(cudaGetLastError());
-    });
+        });
+        return;
+    }
+    if (!ks.hi_merge) {
+        timed_launch(ctx, cls, 1, [&] {
+            const int64_t items = ks.hi_vpw ? (cnt + ks.hi_vpw - 1) / ks.hi_vpw * 32 : cnt;
+            ks.hi<<<grid_for(items, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(aa, list, cnt, round0);
+            CUDA_TRY(cudaGetLastError());
+        });
+        return;
+    }
+    for (int64_t b = 0; b < cnt; b += kHiSlice) {
+        const int64_t c = std::min(kHiSlice, cnt - b);
+        const int32_t *l = list + b;
+        timed_launch(ctx, cls, 3, [&] {
+            ks.hi<<<grid_for(c * 32, ks.hi_threads), ks.hi_threads, 0, ctx->stream>>>(aa, l, c, round0);
+            ks.hi_merge<<<grid_for(c, kThreads), kThreads, 0, ctx->stream>>>(aa, l, c, round0);
+            ks.hi_finish<<<grid_for(c * 32, kThreads), kThreads, 0, ctx->stream>>>(aa, l, c, round0);
+            CUDA_TRY(cudaGetLastError());
+        });
+    }
 }
 
 // Giants: gather then replay; `slots` index bin_giant.  They are a handful
