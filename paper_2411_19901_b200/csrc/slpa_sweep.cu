@@ -529,7 +529,13 @@ void launch_lane(slpa_ctx *ctx, const KernelSet &ks, int which, const SweepArgs 
 // scratch stays at kHiSlice x 2 KB (128 MB) instead of scaling with the bin
 // (1.1 GB at RMAT s24).  Any evaluation order within a round reaches the same
 // fixpoint; a later slice simply sees an earlier one's labels.
-constexpr int64_t kHiSlice = 65536;
+int64_t hi_slice() {
+    static const int64_t m = [] {
+        const char *e = getenv("SLPA_HI_SLICE");
+        return e ? atoll(e) : 65536LL;
+    }();
+    return m;
+}
 
 void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
                int cls) {
@@ -538,6 +544,7 @@ void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int
     const bool small = ks.hi_small && cnt <= hi_small_max();
     if (ks.hi_merge && !small) {
         WorkBuffers &wb = ctx->wb;
+        const int64_t kHiSlice = hi_slice();
         const int64_t cap = std::min<int64_t>(std::max<int64_t>(ctx->g.n_hi, 1), kHiSlice);
         wb.hparts.alloc((size_t)cap * kLpmWords);
         wb.hmeta.alloc((size_t)cap);
@@ -559,6 +566,7 @@ void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int
         });
         return;
     }
+    const int64_t kHiSlice = hi_slice();
     for (int64_t b = 0; b < cnt; b += kHiSlice) {
         const int64_t c = std::min(kHiSlice, cnt - b);
         const int32_t *l = list + b;
