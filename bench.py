@@ -452,6 +452,7 @@ def main():
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
+    e2e_labels = None
     host_graph = None
     int_path = False
     if (rank == 0 or world > 1) and not args.no_e2e:
@@ -491,6 +492,7 @@ def main():
             e2e_val = float(b.item()) / float(a.item())
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": e2e_steps, "s_per_step": e2e_t / e2e_steps}
+        e2e_labels = res.labels
 
     cpu, parity, quality = None, None, None
     if rank == 0 and world == 1 and host_graph is not None:
@@ -511,6 +513,7 @@ def main():
             if args.mode == "det":
                 parity = {"vs": "oracle port: complete sequential lpa_run on the same graph",
                           "labels_equal": bool(np.array_equal(labels_gpu, ref.labels)),
+                          "e2e_labels_equal": bool(np.array_equal(e2e_labels, ref.labels)),
                           "delta_history_equal": delta_gpu == ref.delta_history,
                           "iterations_equal": it_gpu == ref.iterations, "converged_equal": conv_gpu == ref.converged}
             else:

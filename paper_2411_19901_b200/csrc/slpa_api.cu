@@ -42,6 +42,8 @@ int32_t guard(slpa_ctx *ctx, F &&f) {
 
 void require_graph(slpa_ctx *ctx) { SLPA_REQUIRE(ctx->g.base.off.p != nullptr, SLPA_ENOGRAPH, "no graph uploaded"); }
 
+constexpr int64_t kPipeChunk = 1LL << 25;  // arcs per pipelined upload chunk (128 MB of targets)
+
 void upload_csr(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *off, const int32_t *tgt, const void *w,
                 int32_t w_f64, cudaMemcpyKind kind) {
     SLPA_REQUIRE(n >= 0 && m >= 0, SLPA_EINVAL, "negative size");
@@ -58,23 +60,56 @@ void upload_csr(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *off, const i
     g.base.m = m;
     g.base.off.alloc(n + 1);
     g.base.tgt.alloc(m);
-    CUDA_TRY(cudaMemcpyAsync(g.base.off.p, off, (n + 1) * sizeof(int64_t), kind, s));
-    if (m) CUDA_TRY(cudaMemcpyAsync(g.base.tgt.p, tgt, m * sizeof(int32_t), kind, s));
     if (w_f64) {
         g.base.w32.release();
         g.base.w64.alloc(m);
-        if (m) CUDA_TRY(cudaMemcpyAsync(g.base.w64.p, w, m * sizeof(double), kind, s));
     } else {
         g.base.w64.release();
         g.base.w32.alloc(m);
-        if (m) CUDA_TRY(cudaMemcpyAsync(g.base.w32.p, w, m * sizeof(float), kind, s));
     }
     g.n = n;
     g.m = m;
     g.w_f64 = w_f64 ? 1 : 0;
-    slpa_graph_validate(ctx, g.base, g.w_f64);
     ctx->have_labels = 0;
     ctx->part = 0;
+    ctx->pre_checks_valid = 0;
+    const size_t wb = w_f64 ? sizeof(double) : sizeof(float);
+    void *wdst = w_f64 ? (void *)g.base.w64.p : (void *)g.base.w32.p;
+    if (kind != cudaMemcpyHostToDevice || m < kPipeChunk) {
+        CUDA_TRY(cudaMemcpyAsync(g.base.off.p, off, (n + 1) * sizeof(int64_t), kind, s));
+        if (m) CUDA_TRY(cudaMemcpyAsync(g.base.tgt.p, tgt, m * sizeof(int32_t), kind, s));
+        if (m) CUDA_TRY(cudaMemcpyAsync(wdst, w, m * wb, kind, s));
+        slpa_graph_validate(ctx, g.base, g.w_f64);
+        return;
+    }
+    // Pipelined host upload: the arcs travel in chunks on the copy stream
+    // while the compute stream validates each landed chunk and runs the
+    // symmetry / integer-weight / degree checks on it (graph.py:55-68 and
+    // the finalize pass), so those passes hide behind the PCIe transfer.
+    DevBuf<unsigned long long> acc;
+    acc.alloc(9);  // 8 check words + validation flags
+    unsigned *err = reinterpret_cast<unsigned *>(acc.p + 8);
+    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 9 * sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemcpyAsync(g.base.off.p, off, (n + 1) * sizeof(int64_t), kind, s));
+    slpa_validate_offsets_async(ctx, g.base, err);
+    CUDA_TRY(cudaEventRecord(ctx->cev, s));  // the copies overwrite buffers earlier work may still read
+    CUDA_TRY(cudaStreamWaitEvent(ctx->cstream, ctx->cev, 0));
+    for (int64_t e0 = 0; e0 < m; e0 += kPipeChunk) {
+        const int64_t e1 = std::min(m, e0 + kPipeChunk);
+        CUDA_TRY(cudaMemcpyAsync(g.base.tgt.p + e0, tgt + e0, (e1 - e0) * sizeof(int32_t), kind, ctx->cstream));
+        CUDA_TRY(cudaMemcpyAsync((char *)wdst + e0 * wb, (const char *)w + e0 * wb, (e1 - e0) * wb, kind,
+                                 ctx->cstream));
+        CUDA_TRY(cudaEventRecord(ctx->cev, ctx->cstream));
+        CUDA_TRY(cudaStreamWaitEvent(s, ctx->cev, 0));
+        slpa_validate_arcs_range(ctx, g.base, g.w_f64, e0, e1, err);
+        slpa_arc_checks_range(ctx, g.base, g.w_f64, e0, e1, acc.p);
+    }
+    unsigned long long h[9];
+    CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    slpa_throw_validation((unsigned)h[8]);
+    for (int i = 0; i < 8; ++i) ctx->pre_checks[i] = h[i];
+    ctx->pre_checks_valid = 1;  // consumed by slpa_graph_finalize (no visiting order)
 }
 }  // namespace
 
@@ -216,6 +251,8 @@ int32_t slpa_create(int32_t device, slpa_ctx **out) {
             CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
             CUDA_TRY(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_hi));
             CUDA_TRY(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
+            CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->cev, cudaEventDisableTiming));
             CUDA_TRY(cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming));
         } catch (...) {
             delete c;
@@ -268,6 +305,11 @@ int32_t slpa_destroy(slpa_ctx *ctx) {
         cudaStreamSynchronize(ctx->stream2);
         cudaStreamDestroy(ctx->stream2);
     }
+    if (ctx->cev) cudaEventDestroy(ctx->cev);
+    if (ctx->cstream) {
+        cudaStreamSynchronize(ctx->cstream);
+        cudaStreamDestroy(ctx->cstream);
+    }
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return SLPA_OK;
@@ -282,8 +324,16 @@ int32_t slpa_stream(slpa_ctx *ctx, uint64_t *stream_out) {
 int32_t slpa_graph_upload(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *offsets, const int32_t *targets,
                           const void *weights, int32_t weights_f64, const int64_t *order) {
     return guard(ctx, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
         upload_csr(ctx, n, m, offsets, targets, weights, weights_f64, cudaMemcpyHostToDevice);
+        const auto t1 = std::chrono::steady_clock::now();
         slpa_graph_apply_order(ctx, order, false);
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (getenv("SLPA_TRACE")) {
+            const auto t2 = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            fprintf(stderr, "[slpa] upload phases: copy+validate %.2f ms, finalize %.2f ms\n", ms(t0, t1), ms(t1, t2));
+        }
     });
 }
 

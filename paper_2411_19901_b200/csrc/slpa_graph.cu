@@ -458,9 +458,11 @@ __device__ __forceinline__ int64_t row_of(const int64_t *off, int64_t lo, int64_
 template <class W>
 __global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const int32_t *tgt, const W *w, int64_t n,
                                                     int64_t m, unsigned long long *acc, unsigned *bad,
-                                                    unsigned long long *wmax, unsigned long long *dmax) {
+                                                    unsigned long long *wmax, unsigned long long *dmax,
+                                                    int64_t e_begin = 0) {
+    // arcs [e_begin, m) -- the whole graph, or one chunk of a pipelined upload
     __shared__ int64_t s_r[2];
-    const int64_t e0 = (int64_t)blockIdx.x * kArcBlock;
+    const int64_t e0 = e_begin + (int64_t)blockIdx.x * kArcBlock;
     if (e0 >= m) return;
     const int64_t e1 = min(m, e0 + kArcBlock);
     if (threadIdx.x == 0) {
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const in
         for (int j = 0; j < kArcPer; ++j) {
             const int64_t e = a0 + j;
             if (e >= e1) break;
-            while (e >= next) {
+            while (e >= next && u < n - 1) {  // (bounded: offsets are validated concurrently)
                 ++u;
                 start = next;
                 next = __ldg(&off[u + 1]);
@@ -547,6 +549,46 @@ void slpa_arc_hash_impl(slpa_ctx *ctx, uint64_t out[4]) {
     for (int i = 0; i < 4; ++i) out[i] = h[i];
 }
 
+// k_arc_checks over arcs [e0, e1) of `c` into acc[0..7] (stream order).
+void slpa_arc_checks_range(slpa_ctx *ctx, const Csr &c, int w_f64, int64_t e0, int64_t e1, unsigned long long *acc) {
+    if (e1 <= e0) return;
+    const unsigned blocks = (unsigned)((e1 - e0 + kArcBlock - 1) / kArcBlock);
+    cudaStream_t s = ctx->stream;
+    if (w_f64)
+        k_arc_checks<double><<<blocks, 256, 0, s>>>(c.off.p, c.tgt.p, c.w64.p, c.n, e1, acc, (unsigned *)(acc + 4),
+                                                      acc + 5, acc + 6, e0);
+    else
+        k_arc_checks<float><<<blocks, 256, 0, s>>>(c.off.p, c.tgt.p, c.w32.p, c.n, e1, acc, (unsigned *)(acc + 4),
+                                                     acc + 5, acc + 6, e0);
+    CUDA_TRY(cudaGetLastError());
+}
+
+// k_validate_arcs over arcs [e0, e1) (stream order; flags into err).
+void slpa_validate_arcs_range(slpa_ctx *ctx, const Csr &c, int w_f64, int64_t e0, int64_t e1, unsigned *err) {
+    if (e1 <= e0) return;
+    if (w_f64)
+        k_validate_arcs<double><<<grid_for(e1 - e0, kT), kT, 0, ctx->stream>>>(c.tgt.p + e0, c.w64.p + e0, c.n,
+                                                                                e1 - e0, err);
+    else
+        k_validate_arcs<float><<<grid_for(e1 - e0, kT), kT, 0, ctx->stream>>>(c.tgt.p + e0, c.w32.p + e0, c.n,
+                                                                               e1 - e0, err);
+    CUDA_TRY(cudaGetLastError());
+}
+
+// Offsets check of a freshly copied CSR (flags into err; stream order).
+void slpa_validate_offsets_async(slpa_ctx *ctx, const Csr &c, unsigned *err) {
+    k_validate_offsets<<<grid_for(c.n + 1, kT), kT, 0, ctx->stream>>>(c.off.p, c.n, c.m, err);
+    CUDA_TRY(cudaGetLastError());
+}
+
+void slpa_throw_validation(unsigned e) {
+    if (e & 1) throw SlpaError{SLPA_EINVAL, "offsets must be a 1-d array starting at 0"};
+    if (e & 2) throw SlpaError{SLPA_EINVAL, "offsets must be non-decreasing"};
+    if (e & 4) throw SlpaError{SLPA_EINVAL, "offsets[-1] must equal the arc count"};
+    if (e & 8) throw SlpaError{SLPA_EINVAL, "arc target out of range"};
+    if (e & 16) throw SlpaError{SLPA_EINVAL, "arc weights must be positive"};
+}
+
 // Symmetry check + reverse CSR of the active numbering; resets the bins.
 void slpa_graph_finalize(slpa_ctx *ctx) {
     DeviceGraph &g = ctx->g;
@@ -559,23 +601,22 @@ void slpa_graph_finalize(slpa_ctx *ctx) {
     g.rsrc.release();
     g.symmetric = 1;
     g.int_weights = 1;
+    const bool pre = ctx->pre_checks_valid;
+    ctx->pre_checks_valid = 0;
     if (g.n == 0 || g.m == 0) return;
-    // acc: 4 hashes, bad flag, max weight, max degree (one readback)
-    DevBuf<unsigned long long> acc;
-    acc.alloc(8);
-    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 8 * sizeof(unsigned long long), s));
-    const unsigned blocks = (unsigned)((g.m + kArcBlock - 1) / kArcBlock);
-    if (g.w_f64)
-        k_arc_checks<double><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const double *)g.w(), g.n, g.m, acc.p,
-                                                      (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
-    else
-        k_arc_checks<float><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const float *)g.w(), g.n, g.m, acc.p,
-                                                     (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
-    CUDA_TRY(cudaGetLastError());
+    // acc: 4 hashes, bad flag, max weight, max degree (one readback); a
+    // pipelined upload computed them while the arcs were copied
     unsigned long long h[8];
-    CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    acc.release();
+    if (pre) {
+        for (int i = 0; i < 8; ++i) h[i] = ctx->pre_checks[i];
+    } else {
+        DevBuf<unsigned long long> acc;
+        acc.alloc(8);
+        CUDA_TRY(cudaMemsetAsync(acc.p, 0, 8 * sizeof(unsigned long long), s));
+        slpa_arc_checks_range(ctx, g.act(), g.w_f64, 0, g.m, acc.p);
+        CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
     g.symmetric = (h[0] == h[1]) && (h[2] == h[3]);
     g.max_deg = (int64_t)h[6];
     // integer sketch values need integral weights and every weighted degree
@@ -615,6 +656,7 @@ void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order, bool on_device)
         slpa_graph_finalize(ctx);
         return;
     }
+    ctx->pre_checks_valid = 0;  // the checks run on the permuted CSR (the reverse CSR must be built in it)
     const int64_t n = g.n, m = g.m;
     DevBuf<int64_t> d_order;
     const int64_t *ord = order;

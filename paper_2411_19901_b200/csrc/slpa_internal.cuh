@@ -222,6 +222,10 @@ struct slpa_ctx {
     DevBuf<int32_t> lmap_table;
     int32_t zkey = 0;  // internal value of label 0
     int64_t xs_key = 0, xs_units = 0;      // layout of wb.xscratch (exact table size or -k; units)
+    cudaStream_t cstream = nullptr;        // host->device copies of a pipelined upload
+    cudaEvent_t cev = nullptr;             //   (chunk copied)
+    unsigned long long pre_checks[8] = {}; // arc checks computed during the upload (see slpa_graph_finalize)
+    int32_t pre_checks_valid = 0;
     int32_t l2_saved = 0;      // set_label_l2_window changed the process's persisting set-aside
     size_t l2_prev_limit = 0;  //   ... which was this before
     // multi-GPU partition
@@ -270,6 +274,10 @@ static inline bool slpa_large_k(const slpa_config *cfg) {
 void slpa_validate_config(const slpa_config *cfg);
 void slpa_ensure_bins(slpa_ctx *ctx, const slpa_config *cfg);
 void slpa_graph_finalize(slpa_ctx *ctx);  // symmetry check, reverse CSR, reset bins
+void slpa_arc_checks_range(slpa_ctx *ctx, const Csr &c, int w_f64, int64_t e0, int64_t e1, unsigned long long *acc);
+void slpa_validate_arcs_range(slpa_ctx *ctx, const Csr &c, int w_f64, int64_t e0, int64_t e1, unsigned *err);
+void slpa_validate_offsets_async(slpa_ctx *ctx, const Csr &c, unsigned *err);
+void slpa_throw_validation(unsigned e);
 void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order_host_or_dev, bool on_device);
 void slpa_alloc_work(slpa_ctx *ctx);
 void slpa_assemble_unit_edges(slpa_ctx *ctx, int64_t n, int64_t num_edges, uint32_t *d_src, uint32_t *d_dst);
