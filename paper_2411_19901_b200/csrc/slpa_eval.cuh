@@ -266,7 +266,7 @@ __device__ __forceinline__ void lane_stream_u(const SweepArgs &a, int64_t start,
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             L[j] = 0;
-            if (t[j] != v) L[j] = gather_word<DET>(a, t[j], v);
+            if (t[j] != v) L[j] = a.ident ? (uint32_t)t[j] : gather_word<DET>(a, t[j], v);
         }
         const int64_t nx = x0 + kBatch;
         int32_t tn[kBatch];
@@ -388,7 +388,7 @@ __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, i
             inr |= (unsigned)in << j;
             ok |= (unsigned)valid << j;
             L[j] = 0;
-            if (valid) L[j] = gather_word<DET>(a, t[j], v);
+            if (valid) L[j] = a.ident ? (uint32_t)t[j] : gather_word<DET>(a, t[j], v);
         }
         const int64_t nb = b + kBatch;
         int32_t tn[kBatch];

@@ -114,6 +114,9 @@ struct SweepArgs {
     double *xtot;                     //   exact: the tables' binary64 totals (keys in xs)
     int64_t xdeg_lo, xdeg_hi;         //   exact: this launch takes the vertices with xdeg_lo < degree <= xdeg_hi
     int32_t zkey;                     // internal value of label 0 (0 unless caller labels were remapped)
+    int32_t ident;                    // det round 0 of lpa_run's first sweep, no visiting order: every label
+                                      // still equals its vertex id and no word has a changed bit, so the
+                                      // light kernels read a neighbour's label as its id (no gather)
 };
 
 enum { CNT_LO = 0, CNT_HI = 1, CNT_DELTA = 2, CNT_EVALS = 3, CNT_ARCS = 4, CNT_EVALS_HI = 5, CNT_ARCS_HI = 6, CNT_MID = 7, CNT_GIANT = 8, CNT_GPEND = 9, CNT_N = 10 };
@@ -221,6 +224,7 @@ struct slpa_ctx {
     int64_t lmap_shift = 0, lmap_n = 0;
     DevBuf<int32_t> lmap_table;
     int32_t zkey = 0;  // internal value of label 0
+    int32_t labels_initial = 0;  // labels are the ids lpa_run starts from (no sweep since slpa_init_labels)
     int64_t xs_key = 0, xs_units = 0;      // layout of wb.xscratch (exact table size or -k; units)
     cudaStream_t cstream = nullptr;        // host->device copies of a pipelined upload
     cudaEvent_t cev = nullptr;             //   (chunk copied)

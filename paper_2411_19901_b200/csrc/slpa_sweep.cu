@@ -928,6 +928,8 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     const int64_t n = g.n;
     const KernelSet ks = kernels_for(ctx, cfg, true);
     const SweepArgs a = make_args(ctx, cfg, pickless);
+    SweepArgs a_r0 = a;  // round 0 of the first sweep: labels are still the ids (SweepArgs::ident)
+    a_r0.ident = ctx->labels_initial && !g.has_order && ctx->lmap_mode == 0;
     CUDA_TRY(cudaMemsetAsync(wb.counters.p, 0, CNT_TOTAL * sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(wb.flag_b.p, 0, (size_t)n, s));
     for (int c = 0; c < CNT_N; ++c) ctx->h_sum[c] = 0;
@@ -970,10 +972,11 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         unsigned long long nf = 0;
         CUDA_TRY(cudaMemcpyAsync(&nf, c0, sizeof(nf), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
-        launch_lane(ctx, ks, 0, a, wb.wl_lo.p, (int64_t)nf, 1, SLPA_PROF_EVAL_LO0);
+        launch_lane(ctx, ks, 0, a_r0, wb.wl_lo.p, (int64_t)nf, 1, SLPA_PROF_EVAL_LO0);
     } else {
-        launch_lane(ctx, ks, 0, a, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
+        launch_lane(ctx, ks, 0, a_r0, g.bin_lo.p, g.n_lo, 1, SLPA_PROF_EVAL_LO0);
     }
+    ctx->labels_initial = 0;
     int64_t rounds = 1;
     unsigned long long evals0 = 0, arcs0 = 0;
     bool first = true;
@@ -1200,6 +1203,7 @@ int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     read_counters(ctx);
     const int64_t ev = (int64_t)(ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI]);
     const int64_t ar = (int64_t)(ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI]);
+    ctx->labels_initial = 0;
     ctx->stats.rounds += 1;
     ctx->stats.vertex_evals += ev;
     ctx->stats.arc_reads += ar;
@@ -1293,6 +1297,7 @@ void map_caller_labels(slpa_ctx *ctx, const int32_t *host_by_id) {
 }
 
 void slpa_init_labels(slpa_ctx *ctx) {
+    ctx->labels_initial = 1;
     ctx->lmap_mode = 0;
     ctx->lmap_shift = 0;
     ctx->zkey = 0;
@@ -1357,6 +1362,7 @@ void slpa_labels_from_host(slpa_ctx *ctx, const int32_t *host) {
         CUDA_TRY(cudaMemcpyAsync(ctx->wb.lab_old.p, host, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
     }
     map_caller_labels(ctx, host);
+    ctx->labels_initial = 0;
     k_sync_lab_new<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.lab_old.p, ctx->wb.lab_new.p, n);
     CUDA_TRY(cudaGetLastError());
 }
