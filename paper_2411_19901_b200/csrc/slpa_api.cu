@@ -324,6 +324,7 @@ int32_t slpa_stream(slpa_ctx *ctx, uint64_t *stream_out) {
 int32_t slpa_graph_upload(slpa_ctx *ctx, int64_t n, int64_t m, const int64_t *offsets, const int32_t *targets,
                           const void *weights, int32_t weights_f64, const int64_t *order) {
     return guard(ctx, [&] {
+        NvtxRange nvtx_upload("slpa graph upload");
         const auto t0 = std::chrono::steady_clock::now();
         upload_csr(ctx, n, m, offsets, targets, weights, weights_f64, cudaMemcpyHostToDevice);
         const auto t1 = std::chrono::steady_clock::now();
@@ -428,6 +429,7 @@ int32_t slpa_validate_graph(slpa_ctx *ctx, int32_t *code, int64_t *vertex, doubl
 int32_t slpa_run(slpa_ctx *ctx, const slpa_config *cfg, int32_t *labels_out, int64_t *delta_history,
                  int32_t *iterations, int32_t *converged, slpa_hook_fn hook, void *hook_user) {
     return guard(ctx, [&] {
+        NvtxRange nvtx_run("slpa lpa_run");
         slpa_validate_config(cfg);
         require_graph(ctx);
         SLPA_REQUIRE(delta_history && iterations && converged, SLPA_EINVAL, "output pointers are NULL");

@@ -16,7 +16,17 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <nvtx3/nvToolsExt.h>
 #include "../../include/slpa.h"
+
+// NVTX ranges (lpa_run / sweep / round / commit / upload) for Nsight timelines;
+// header-only NVTX3, no cost without an attached tool.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 #define SLPA_CHG 0x80000000u
 #define SLPA_LMASK 0x7fffffffu

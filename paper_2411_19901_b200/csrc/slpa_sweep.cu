@@ -831,6 +831,7 @@ __global__ void k_iota(int32_t *out, int64_t n) {
 // other speculation, so the fixpoint is still the sequential sweep.  Heavy
 // vertices are not deferred (a round-local policy would need a global vote).
 void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickless, int round) {
+    NvtxRange nvtx_round("slpa partitioned round");
     DeviceGraph &g = ctx->g;
     WorkBuffers &wb = ctx->wb;
     cudaStream_t s = ctx->stream;
@@ -922,6 +923,7 @@ int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg) {
 
 // ====================================================================== drivers
 int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
+    NvtxRange nvtx_sweep("slpa sweep (deterministic)");
     DeviceGraph &g = ctx->g;
     WorkBuffers &wb = ctx->wb;
     cudaStream_t s = ctx->stream;
@@ -1006,6 +1008,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         CUDA_TRY(cudaGetLastError());
     }
     for (;;) {
+        NvtxRange nvtx_round("slpa round");
         if (agiant) {
             if (g_inflight && cudaEventQuery(ctx->gev1) == cudaSuccess) {
                 k_or_clear<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_g.p, wb.dirty_a.p, nwords);
@@ -1122,6 +1125,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     giant_join(ctx);
     const unsigned long long evals = ctx->h_sum[CNT_EVALS] + ctx->h_sum[CNT_EVALS_HI];
     const unsigned long long arcs = ctx->h_sum[CNT_ARCS] + ctx->h_sum[CNT_ARCS_HI];
+    NvtxRange nvtx_commit("slpa commit");
     // commit: L0 <- L1, delta, next-sweep flags pushed from the changed rows
     const int64_t fwords = (n + 31) / 32;
     CUDA_TRY(cudaMemsetAsync(wb.fbits.p, 0, (size_t)fwords * sizeof(uint32_t), s));
@@ -1178,6 +1182,7 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
 }
 
 int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
+    NvtxRange nvtx_sweep("slpa sweep (async)");
     DeviceGraph &g = ctx->g;
     WorkBuffers &wb = ctx->wb;
     cudaStream_t s = ctx->stream;

@@ -144,6 +144,31 @@ def test_move_raises_like_reference(slpa, eng, name):
         slpa.lpa_move(g, labels, flags, cfg, G.meta(name)["pickless"], engine=eng)
 
 
+@pytest.mark.parametrize("variant", ["mg", "bm"])
+def test_move_negative_labels_rmat_vs_oracle(slpa, eng, oracle, variant):
+    """lpa_move on caller labels spanning the whole int32 range (the rank
+    map) and on shifted negative labels (the shift map) equals the sequential
+    reference on an RMAT graph with high-degree rows."""
+    eng.gen_rmat(15, seed=44, permute=True)
+    off, tgt, w = eng.download()
+    from golden_io import GoldenGraph
+    g = GoldenGraph(off, tgt, w)
+    n = g.num_vertices
+    rng = np.random.default_rng(7)
+    cfg = slpa.LpaConfig(variant=variant)
+    for labels in (rng.integers(-2**31, 2**31 - 1, n).astype(np.int32),   # span > 2^31: rank map
+                   (np.arange(n) - n // 2).astype(np.int32)):            # shift map
+        flags = rng.random(n) < 0.9
+        for pickless in (True, False):
+            lab_ref, fl_ref = labels.copy(), flags.copy()
+            d_ref = oracle.lpa_move(g, lab_ref, fl_ref, cfg, pickless)
+            lab, fl = labels.copy(), flags.copy()
+            d = eng.move(cfg, lab, fl, pickless)
+            assert d == d_ref
+            np.testing.assert_array_equal(lab, lab_ref)
+            np.testing.assert_array_equal(fl, fl_ref)
+
+
 def test_hook_exception_propagates(slpa, eng):
     g = slpa.build_graph(4, [(0, 1), (1, 2), (2, 3)], engine=eng)
 
@@ -219,6 +244,9 @@ CFG_MATRIX = [
     dict(variant="mg", partial_groups=64),
     dict(variant="bm", partial_groups=48),
     dict(variant="mg", shared_sketch=True),
+    dict(variant="mg", sketch_slots=40),                          # large-k kernel (chunked rows, k > 32)
+    dict(variant="mg", sketch_slots=100, scan_mode="double"),     # large-k kernel, k > 64
+    dict(variant="exact"),                                        # warp hash tables, both degree tiers at s17
 ]
 
 
