@@ -388,7 +388,14 @@ __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, i
             inr |= (unsigned)in << j;
             ok |= (unsigned)valid << j;
             L[j] = 0;
-            if (valid) L[j] = a.ident ? (uint32_t)t[j] : gather_word<DET>(a, t[j], v);
+            if (valid)
+                L[j] = a.ident ? (uint32_t)t[j]
+                               : (DET && !a.lo_direct ? __ldcg(&a.lab_new[t[j]]) : gather_word<DET>(a, t[j], v));
+        }
+        if (DET && !a.lo_direct && !a.ident) {  // lab_new-first: a changed higher neighbour's L0
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (((ok >> j) & 1u) && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
         }
         const int64_t nb = b + kBatch;
         int32_t tn[kBatch];

@@ -346,6 +346,11 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     a.tbits = ctx->prof_on ? ctx->wb.tbits.p : nullptr;
     a.fbits = ctx->wb.fbits.p;
     a.zkey = ctx->zkey;
+    static const int lo_direct = [] {
+        const char *e = getenv("SLPA_LO_DIRECT");
+        return e ? atoi(e) : 0;
+    }();
+    a.lo_direct = lo_direct;
     a.giant_bin = g.bin_giant.p;
     a.giant_off = g.giant_off.p;
     a.glab = ctx->wb.glab.p;
