@@ -434,7 +434,7 @@ def main():
     achieved = alg_bytes / (dom["ms"] / 1000.0) / 1e9 if dom["ms"] > 0 else 0.0
     peak, peak_src = peaks()
     total_ms = sum(v["ms"] for v in prof.values())
-    traffic, traffic_run = None, None
+    traffic, traffic_run, sectors_per_request = None, None, None
     tfile = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):  # tools/ncu_traffic.py over an ncu capture of ONE lpa_run of this workload
         with open(tfile) as f:
@@ -445,6 +445,7 @@ def main():
             if c and dom["launches"]:
                 traffic_run = c["dram_bytes_per_run"]
                 traffic = traffic_run / dom["launches"]  # same launch count as alg_bytes_per_launch
+                sectors_per_request = c.get("ld_sectors_per_request")
     # run level: bytes of the vertices each sweep processes
     # (first evaluation only: re-evaluations are overhead) over the whole run
     run_alg = ALG_BYTES_PER_VERTEX * st_prof["first_evals"] + ALG_BYTES_PER_ARC * st_prof["first_arcs"]
@@ -547,6 +548,8 @@ def main():
                          "alg_bytes_per_launch": alg_bytes / max(dom["launches"], 1),
                          "launches_per_run": dom["launches"],
                          "alg_bytes_per_run": alg_bytes, "traffic_per_run": traffic_run,
+                         "traffic_over_alg": (traffic_run / alg_bytes) if traffic_run and alg_bytes else None,
+                         "ld_sectors_per_request": sectors_per_request,
                          "ms_per_launch": dom["ms"] / max(dom["launches"], 1),
                          "share_of_step": dom["ms"] / total_ms if total_ms else None,
                          "run_alg_bytes": run_alg, "run_achieved": run_achieved, "run_frac": run_achieved / peak,

@@ -764,6 +764,13 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
         if (lane == 0) a.flag_cur[v] = 0;
     }
     const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    if (a.pf && lane < 2) {  // one bulk L2 prefetch per array: the 32 lanes' chunk streams then hit L2
+        const char *base = lane == 0 ? (const char *)(a.tgt + lo) : (const char *)a.w + lo * (int64_t)sizeof(W);
+        const uint64_t b0 = (uint64_t)base & ~(uint64_t)15;
+        const uint64_t b1 = ((uint64_t)base + (uint64_t)(hi - lo) * 4u + 15u) & ~(uint64_t)15;
+        if (sizeof(W) == 4 && b1 > b0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((unsigned)(b1 - b0)) : "memory");
+    }
     const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     MgSketchDev<8, V> part;
     part.reset(8, a.zkey);
@@ -772,9 +779,7 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
     bool lc = false;
     if (a.stream == 1)
         lane_stream_p<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
-            if (a.dbg & 2) {  // timing experiment only: the streams without the sketch
-                if (valid) part.s[0] += (uint32_t)c ^ (uint32_t)w;
-            } else if (valid) part.acc(c, (V)w, 8);
+            if (valid) part.acc(c, (V)w, 8);
         });
     else
         lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {

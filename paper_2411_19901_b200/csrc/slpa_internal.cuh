@@ -124,6 +124,7 @@ struct SweepArgs {
     double *xtot;                     //   exact: the tables' binary64 totals (keys in xs)
     int64_t xdeg_lo, xdeg_hi;         //   exact: this launch takes the vertices with xdeg_lo < degree <= xdeg_hi
     int32_t zkey;                     // internal value of label 0 (0 unless caller labels were remapped)
+    int32_t pf;                       // heavy scan: bulk L2 prefetch of the row (SLPA_HI_PREFETCH)
     int32_t lo_direct;                // light rows: 1 gather a higher neighbour's L0 directly, 0 lab_new + fix-up
     int32_t ident;                    // det round 0 of lpa_run's first sweep, no visiting order: every label
                                       // still equals its vertex id and no word has a changed bit, so the

@@ -351,6 +351,11 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
         return e ? atoi(e) : 0;
     }();
     a.lo_direct = lo_direct;
+    static const int pf = [] {
+        const char *e = getenv("SLPA_HI_PREFETCH");
+        return e ? atoi(e) : 1;
+    }();
+    a.pf = pf;
     a.giant_bin = g.bin_giant.p;
     a.giant_off = g.giant_off.p;
     a.glab = ctx->wb.glab.p;

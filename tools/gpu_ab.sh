@@ -1,9 +1,7 @@
-# A/B: L2 persisting set-aside for the label words (device ms per run, RMAT s24 det)
+# A/B: bulk L2 prefetch of heavy rows (device ms per run + first k_mg_hi_scan launch, RMAT s24 det)
 mkdir -p gpurun_out
-run() { echo "=== $*"; env "$@" timeout 300 python tools/prof_run.py --scale 24 --runs 4 2>&1 | grep -E "^run [23]"; }
+run() { echo "=== $*"; env "$@" timeout 300 python tools/prof_run.py --scale 24 --runs 5 2>&1 | grep -E "^run [234]"; env "$@" timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none --cache-control none -k regex:k_mg_hi_scan -c 1 python tools/prof_run.py --scale 24 --runs 1 2>&1 | grep -E "gpu__time|dram__bytes"; }
 {
-run SLPA_L2_PERSIST_MB=4096
-run SLPA_L2_PERSIST_MB=0
-run SLPA_L2_PERSIST_MB=32
-run SLPA_L2_PERSIST_MB=48
+run SLPA_HI_PREFETCH=0
+run SLPA_HI_PREFETCH=1
 } > gpurun_out/ab.log 2>&1
