@@ -301,11 +301,12 @@ def run_partitioned(args, world, rank, local, dist):
     clocks = ClockSampler(local)
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters_all = []
+    iters_all, xstats = [], []
     ev0.record()
     for _ in range(args.steps):
         res = lpa_run_partitioned(eng, cfg, ranges)
         iters_all.append(res.iterations)
+        xstats.append((res.rounds, res.sparse_rounds, res.exchange_bytes))
     ev1.record()
     barrier()
     clk = clocks.stop()
@@ -328,7 +329,11 @@ def run_partitioned(args, world, rank, local, dist):
                                       f"flag max-reduce on the library stream",
                        "ranges": ranges,
                        "l2_policy": "inputs larger than L2"},
-            "iterations_per_step": iters_all, "gpu_launches": None, "e2e": None, "roofline": None,
+            "iterations_per_step": iters_all,
+            "exchange": {"rounds_per_step": xstats[-1][0], "sparse_rounds_per_step": xstats[-1][1],
+                         "rank0_bytes_per_step": xstats[-1][2],
+                         "dense_bytes_per_round": 4 * (ranges[0][1] - ranges[0][0]) + n},
+            "gpu_launches": None, "e2e": None, "roofline": None,
             "cpu_baseline": None, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

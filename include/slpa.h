@@ -212,6 +212,18 @@ int32_t slpa_part_end_exchange(slpa_ctx *ctx);
 int32_t slpa_part_det_buffers(slpa_ctx *ctx, uint64_t *lab_new_dptr, uint64_t *dirty_bytes_dptr);
 int32_t slpa_part_det_round(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickless, int32_t round);
 int32_t slpa_part_det_import(slpa_ctx *ctx, int64_t *dirty_total);
+/* Sparse round exchange (instead of slpa_part_det_dense + the dense host
+ * collectives + slpa_part_det_import): _collect lists this rank's moved owned
+ * words ((id, word) int32 pairs) followed by its remote dirty marks (ids) in a
+ * device buffer; the host all-gathers every rank's list into recv (rank r at
+ * recv + r * stride int32s, counts[2r] = words, counts[2r+1] = marks) and
+ * _apply writes the remote words, sets the owned marks and returns this rank's
+ * dirty-vertex count (the host sums it over the ranks). */
+int32_t slpa_part_det_collect(slpa_ctx *ctx, uint64_t *list_dptr, int64_t *n_words, int64_t *n_marks);
+int32_t slpa_part_det_apply(slpa_ctx *ctx, uint64_t recv_dptr, int64_t stride, const int64_t *counts, int32_t world,
+                            int32_t self, int64_t *dirty_owned);
+/* Dense round exchange: the dirty bitmap as bytes for a host MAX-reduce. */
+int32_t slpa_part_det_dense(slpa_ctx *ctx);
 int32_t slpa_part_det_commit(slpa_ctx *ctx, const slpa_config *cfg, int64_t *changed_local);
 /* Rank-local tallies: internal weight (scalar) and device float64[n]
  * incident / int64[n] sizes arrays for an all-reduce; then Q from the

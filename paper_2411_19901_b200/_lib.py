@@ -108,6 +108,9 @@ SIGNATURES = {
     "slpa_part_det_buffers": (_i32, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "slpa_part_det_round": (_i32, [_vp, ctypes.POINTER(SlpaConfig), _i32, _i32]),
     "slpa_part_det_import": (_i32, [_vp, ctypes.POINTER(_i64)]),
+    "slpa_part_det_collect": (_i32, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "slpa_part_det_apply": (_i32, [_vp, _u64, _i64, _vp, _i32, _i32, ctypes.POINTER(_i64)]),
+    "slpa_part_det_dense": (_i32, [_vp]),
     "slpa_part_det_commit": (_i32, [_vp, ctypes.POINTER(SlpaConfig), ctypes.POINTER(_i64)]),
     "slpa_part_tally": (_i32, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "slpa_part_modularity": (_i32, [_vp, _d, ctypes.POINTER(_d)]),

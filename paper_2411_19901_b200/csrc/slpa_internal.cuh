@@ -186,7 +186,9 @@ struct WorkBuffers {
     DevBuf<uint8_t> flag_a, flag_b;
     DevBuf<uint32_t> dirty_a, dirty_b;
     DevBuf<uint32_t> dirty_g, dirty_gp;  // asynchronous giants: their marks / marks waiting for them
-    DevBuf<uint8_t> dirty_bytes;  // multi-GPU deterministic: dirty marks exchanged as bytes
+    DevBuf<uint8_t> dirty_bytes;  // multi-GPU deterministic: dirty marks exchanged as bytes (dense rounds)
+    DevBuf<uint32_t> lab_sent;    //   the label words last published (sparse rounds send the ones that moved)
+    DevBuf<int32_t> xlist;        //   this rank's sparse round list: (id, word) pairs, then remote mark ids
     DevBuf<uint32_t> tbits;       // profiling: turn bitmap (the sequential sweep's processed set)
     DevBuf<uint32_t> fbits;       // det commit: next-sweep flag bitmap
     DevBuf<unsigned long long> dcount;
@@ -204,7 +206,7 @@ struct WorkBuffers {
     DevBuf<unsigned char> xscratch; // exact / large-k kernels: per-warp hash-table keys or per-thread sketches
     DevBuf<double> xtotals;         // exact: per-warp hash-table totals
     size_t bytes() const {
-        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() + dirty_g.bytes() + dirty_gp.bytes() +
+        return lab_old.bytes() + lab_new.bytes() + flag_a.bytes() + flag_b.bytes() + dirty_a.bytes() + dirty_bytes.bytes() + lab_sent.bytes() + xlist.bytes() + dirty_g.bytes() + dirty_gp.bytes() +
                dirty_b.bytes() + tbits.bytes() + fbits.bytes() + hparts.bytes() + hmeta.bytes() + wl_lo.bytes() + wl_mid.bytes() + wl_hi.bytes() + wl_giant.bytes() + glab.bytes() + gw.bytes() + io_labels.bytes() + io_flags.bytes() +
                counters.bytes() + metric_d.bytes() + metric_u.bytes() + scratch.bytes() + xscratch.bytes() + xtotals.bytes();
     }
@@ -303,6 +305,10 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless);
 int64_t slpa_sweep_async(slpa_ctx *ctx, const slpa_config *cfg, int pickless);
 void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickless, int round);
 int64_t slpa_part_det_import_impl(slpa_ctx *ctx);
+void slpa_part_det_collect_impl(slpa_ctx *ctx, uint64_t *list_dptr, int64_t *n_words, int64_t *n_marks);
+int64_t slpa_part_det_apply_impl(slpa_ctx *ctx, const int32_t *recv, int64_t stride, const int64_t *counts_host,
+                                 int32_t world, int32_t self);
+void slpa_part_det_dense_impl(slpa_ctx *ctx);
 int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg);
 void slpa_init_labels(slpa_ctx *ctx);  // lab = ids (or arange), flags = 1
 void slpa_labels_to_host(slpa_ctx *ctx, int32_t *host);       // by original id

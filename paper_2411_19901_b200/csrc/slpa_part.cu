@@ -180,13 +180,19 @@ int32_t slpa_part_begin(slpa_ctx *ctx, const slpa_config *cfg) {
         require_part(ctx);
         slpa_ensure_bins(ctx, cfg);
         slpa_alloc_work(ctx);
-        if (cfg->worker_count == 0) ctx->wb.dirty_bytes.alloc((size_t)ctx->g.n);
+        if (cfg->worker_count == 0) {
+            ctx->wb.dirty_bytes.alloc((size_t)ctx->g.n);
+            ctx->wb.lab_sent.alloc((size_t)ctx->g.n);
+        }
         ctx->stats = slpa_run_stats{};
         slpa_init_labels(ctx);
         const int64_t n = ctx->g.n;
         if (ctx->v_begin > 0) CUDA_TRY(cudaMemsetAsync(ctx->wb.flag_a.p, 0, (size_t)ctx->v_begin, ctx->stream));
         if (ctx->v_end < n)
             CUDA_TRY(cudaMemsetAsync(ctx->wb.flag_a.p + ctx->v_end, 0, (size_t)(n - ctx->v_end), ctx->stream));
+        if (cfg->worker_count == 0 && n > 0)  // every replica starts from the same words (the ids)
+            CUDA_TRY(cudaMemcpyAsync(ctx->wb.lab_sent.p, ctx->wb.lab_new.p, (size_t)n * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         ctx->have_labels = 1;
     });
@@ -223,6 +229,33 @@ int32_t slpa_part_det_round(slpa_ctx *ctx, const slpa_config *cfg, int32_t pickl
         SLPA_REQUIRE(ctx->wb.dirty_bytes.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
         slpa_ensure_bins(ctx, cfg);
         slpa_part_det_round_impl(ctx, cfg, pickless ? 1 : 0, round);
+    });
+}
+
+int32_t slpa_part_det_collect(slpa_ctx *ctx, uint64_t *list_dptr, int64_t *n_words, int64_t *n_marks) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        SLPA_REQUIRE(ctx->wb.lab_sent.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
+        SLPA_REQUIRE(list_dptr && n_words && n_marks, SLPA_EINVAL, "NULL argument");
+        slpa_part_det_collect_impl(ctx, list_dptr, n_words, n_marks);
+    });
+}
+
+int32_t slpa_part_det_apply(slpa_ctx *ctx, uint64_t recv_dptr, int64_t stride, const int64_t *counts, int32_t world,
+                            int32_t self, int64_t *dirty_owned) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        SLPA_REQUIRE(counts && dirty_owned && world >= 1 && self >= 0 && self < world, SLPA_EINVAL, "bad arguments");
+        *dirty_owned = slpa_part_det_apply_impl(ctx, reinterpret_cast<const int32_t *>((uintptr_t)recv_dptr), stride,
+                                                counts, world, self);
+    });
+}
+
+int32_t slpa_part_det_dense(slpa_ctx *ctx) {
+    return guard(ctx, [&] {
+        require_part(ctx);
+        SLPA_REQUIRE(ctx->wb.dirty_bytes.p, SLPA_EINVAL, "call slpa_part_begin with worker_count == 0 first");
+        slpa_part_det_dense_impl(ctx);
     });
 }
 

@@ -885,10 +885,154 @@ void slpa_part_det_round_impl(slpa_ctx *ctx, const slpa_config *cfg, int pickles
         launch_lane(ctx, ks, 1, a, wb.wl_mid.p, nmid, 0, SLPA_PROF_EVAL_MIDK);
     }
     giant_join(ctx);
-    if (n > 0) k_dirty_bits_to_bytes<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, wb.dirty_bytes.p, n);
-    CUDA_TRY(cudaGetLastError());
-    // no host sync: the caller's exchange is queued on ctx->stream behind these kernels
+    // no host sync: slpa_part_det_collect (sparse exchange) or
+    // slpa_part_det_dense (dense exchange) follows on ctx->stream
     ctx->stats.rounds += 1;
+}
+
+// ------------------------------------------------------------ sparse round exchange
+// Per round a rank only has to publish (a) the owned label words that moved
+// since its last exchange and (b) the dirty marks it set on remote vertices.
+// slpa_part_det_collect packs both into one int32 list (words as (id, word)
+// pairs, then mark ids); the host all-gathers the lists (padded to the
+// longest) and slpa_part_det_apply writes the remote words into the replica
+// and sets the marks this rank owns.  When the lists would outweigh the dense
+// exchange (4n + n bytes) the host picks slpa_part_det_dense for the round --
+// the choice is made from the all-gathered counts, so every rank agrees.
+__global__ void k_collect_words(const uint32_t *__restrict__ lab_new, uint32_t *__restrict__ lab_sent, int64_t vb,
+                                int64_t ve, int32_t *__restrict__ out, unsigned long long *__restrict__ cursor) {
+    const int64_t v = vb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool moved = false;
+    uint32_t w = 0;
+    if (v < ve) {
+        w = __ldcg(&lab_new[v]);
+        moved = w != lab_sent[v];
+        if (moved) lab_sent[v] = w;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, moved);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(cursor, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (moved) {
+        const int64_t k = (int64_t)base + __popc(m & ((1u << lane) - 1u));
+        out[2 * k] = (int32_t)v;
+        out[2 * k + 1] = (int32_t)w;
+    }
+}
+__device__ __forceinline__ uint32_t owned_bits(int64_t i, int64_t vb, int64_t ve) {  // word i's owned vertices
+    uint32_t own = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int64_t v = i * 32 + b;
+        if (v >= vb && v < ve) own |= 1u << b;
+    }
+    return own;
+}
+// remote dirty marks (bitmap words outside the owned range)
+__global__ void k_collect_marks(const uint32_t *__restrict__ dirty, int64_t nwords, int64_t vb, int64_t ve,
+                                int32_t *__restrict__ out, unsigned long long *__restrict__ cursor) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nwords) return;
+    const uint32_t w = dirty[i];
+    if (!w) return;
+    const uint32_t rem = w & ~owned_bits(i, vb, ve);
+    if (!rem) return;
+    const unsigned long long base = atomicAdd(cursor, (unsigned long long)__popc(rem));
+    int k = 0;
+    for (uint32_t r = rem; r; r &= r - 1, ++k) out[base + k] = (int32_t)(i * 32 + __ffs(r) - 1);
+}
+__global__ void k_apply_lists(const int32_t *__restrict__ recv, int64_t stride, const int64_t *__restrict__ counts,
+                              int32_t world, int32_t self, int64_t vb, int64_t ve, uint32_t *__restrict__ lab_new,
+                              uint32_t *__restrict__ lab_sent_unused, uint32_t *__restrict__ dirty) {
+    const int r = blockIdx.y;
+    if (r == self || r >= world) return;
+    const int64_t nw = counts[2 * r], nm = counts[2 * r + 1];
+    const int32_t *l = recv + (int64_t)r * stride;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nw + nm; x += (int64_t)gridDim.x * blockDim.x) {
+        if (x < nw) {
+            __stcg(&lab_new[l[2 * x]], (uint32_t)l[2 * x + 1]);
+        } else {
+            const int32_t t = l[2 * nw + (x - nw)];
+            if (t >= vb && t < ve) atomicOr(&dirty[t >> 5], 1u << (t & 31));
+        }
+    }
+}
+__global__ void k_clear_remote_bits(uint32_t *__restrict__ dirty, int64_t nwords, int64_t vb, int64_t ve) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nwords && dirty[i]) dirty[i] &= owned_bits(i, vb, ve);
+}
+__global__ void k_count_owned_bits(const uint32_t *__restrict__ bits, int64_t vb, int64_t ve,
+                                   unsigned long long *__restrict__ out) {
+    const int64_t v = vb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool b = v < ve && ((__ldcg(&bits[v >> 5]) >> (v & 31)) & 1u);
+    const unsigned m = __ballot_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(out, (unsigned long long)__popc(m));
+}
+
+void slpa_part_det_collect_impl(slpa_ctx *ctx, uint64_t *list_dptr, int64_t *n_words, int64_t *n_marks) {
+    DeviceGraph &g = ctx->g;
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = g.n, vb = ctx->v_begin, ve = ctx->v_end, nwords = (n + 31) / 32;
+    wb.xlist.alloc((size_t)(2 * (ve - vb) + (n - (ve - vb)) + 1));
+    wb.dcount.alloc(2);
+    CUDA_TRY(cudaMemsetAsync(wb.dcount.p, 0, 2 * sizeof(unsigned long long), s));
+    if (ve > vb)
+        k_collect_words<<<grid_for(ve - vb, kThreads), kThreads, 0, s>>>(wb.lab_new.p, wb.lab_sent.p, vb, ve, wb.xlist.p,
+                                                                         wb.dcount.p);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h[2];
+    CUDA_TRY(cudaMemcpyAsync(h, wb.dcount.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t nw = (int64_t)h[0];
+    if (nwords > 0)
+        k_collect_marks<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, nwords, vb, ve,
+                                                                        wb.xlist.p + 2 * nw, wb.dcount.p + 1);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(h, wb.dcount.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *list_dptr = (uint64_t)(uintptr_t)wb.xlist.p;
+    *n_words = nw;
+    *n_marks = (int64_t)h[1];
+}
+
+int64_t slpa_part_det_apply_impl(slpa_ctx *ctx, const int32_t *recv, int64_t stride, const int64_t *counts_host,
+                                 int32_t world, int32_t self) {
+    DeviceGraph &g = ctx->g;
+    WorkBuffers &wb = ctx->wb;
+    cudaStream_t s = ctx->stream;
+    const int64_t vb = ctx->v_begin, ve = ctx->v_end;
+    DevBuf<int64_t> cnt;
+    cnt.alloc((size_t)2 * world);
+    CUDA_TRY(cudaMemcpyAsync(cnt.p, counts_host, 2 * world * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    const int64_t nwords = (g.n + 31) / 32;
+    if (nwords > 0)  // this rank's marks on remote vertices went out with its list
+        k_clear_remote_bits<<<grid_for(nwords, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, nwords, vb, ve);
+    int64_t most = 0;
+    for (int r = 0; r < world; ++r) most = std::max<int64_t>(most, counts_host[2 * r] + counts_host[2 * r + 1]);
+    if (most > 0) {
+        const dim3 grid((unsigned)std::min<int64_t>(grid_for(most, kThreads), 4096), (unsigned)world);
+        k_apply_lists<<<grid, kThreads, 0, s>>>(recv, stride, cnt.p, world, self, vb, ve, wb.lab_new.p, nullptr,
+                                                wb.dirty_a.p);
+    }
+    wb.dcount.alloc(2);
+    CUDA_TRY(cudaMemsetAsync(wb.dcount.p, 0, sizeof(unsigned long long), s));
+    if (ve > vb) k_count_owned_bits<<<grid_for(ve - vb, kThreads), kThreads, 0, s>>>(wb.dirty_a.p, vb, ve, wb.dcount.p);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, wb.dcount.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return (int64_t)h;
+}
+
+// Dense round exchange: the dirty bitmap as bytes for the host's MAX-reduce
+// (the owned label words travel in the host's all-gather of lab_new).
+void slpa_part_det_dense_impl(slpa_ctx *ctx) {
+    const int64_t n = ctx->g.n;
+    if (n > 0)
+        k_dirty_bits_to_bytes<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(ctx->wb.dirty_a.p,
+                                                                                   ctx->wb.dirty_bytes.p, n);
+    CUDA_TRY(cudaGetLastError());
 }
 
 int64_t slpa_part_det_import_impl(slpa_ctx *ctx) {
@@ -925,6 +1069,8 @@ int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg) {
         k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
     if (n > 0) k_fold_all<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, wb.lab_new.p, n);
     if (n > 0) k_flag_bits_to_bytes<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, s>>>(wb.fbits.p, wb.flag_a.p, n);
+    if (n > 0)  // every rank folded the same words: the published state is the folded one
+        CUDA_TRY(cudaMemcpyAsync(wb.lab_sent.p, wb.lab_new.p, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(cudaGetLastError());
     read_counters(ctx);
     ctx->stats.sweeps += 1;

@@ -15,10 +15,11 @@ SURVEY §8(e2)), per sweep:
 
 Deterministic sweeps (worker_count == 0) run the speculative
 rounds of the single-GPU engine across ranks: per round every
-rank evaluates its owned flagged / dirty vertices, then the owned ranges of
-the speculative label words (lab_new, bit 31 = changed) are all-gathered and
-the dirty marks MAX-reduced (as bytes: the OR); the sweep ends when no mark is
-set anywhere.  Stale remote reads are re-evaluated through the marks like any
+rank evaluates its owned flagged / dirty vertices, then publishes the owned
+speculative label words (lab_new, bit 31 = changed) that moved and the dirty
+marks it set on other ranks' vertices -- as changed-only lists when they are
+short (most rounds), else densely (the owned ranges all-gathered, the marks
+MAX-reduced as bytes); the sweep ends when no mark is set anywhere.  Stale remote reads are re-evaluated through the marks like any
 other speculation, so labels, delta history and iteration count are
 bit-identical to the sequential reference (lpa.py:204-224).
 
@@ -99,6 +100,9 @@ class PartitionedResult:
     iterations: int
     delta_history: list = field(default_factory=list)
     converged: bool = False
+    rounds: int = 0                  # deterministic: speculative rounds over all sweeps
+    sparse_rounds: int = 0           #   of which exchanged changed-only lists
+    exchange_bytes: int = 0          #   bytes this rank contributed to the round exchanges
 
 
 def _sync(t):
@@ -149,7 +153,49 @@ def confirm_symmetric(engine, group=None) -> bool:
     return sym
 
 
-def _det_sweep(engine, cfg, pickless, ex, lab_new, dirty) -> int:
+def _det_round_exchange(engine, ex, lab_new, dirty, on_lib, mode, stats=None) -> int:
+    """One round's exchange; returns the global dirty-vertex count.
+
+    sparse: every rank publishes the owned label words that moved since its
+    last exchange and the marks it set on remote vertices (one all-gather of
+    padded int32 lists); dense: the owned ranges of the label words are
+    all-gathered and the dirty marks MAX-reduced as bytes.  "auto" picks the
+    sparse exchange unless the longest list would move more bytes than the
+    dense one -- decided from the all-gathered counts, so every rank agrees."""
+    import torch
+    lst, nw, nm = engine.part_det_collect()
+    dev = lab_new.device
+    counts = torch.tensor([nw, nm], dtype=torch.int64, device=dev)
+    allc = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(ex.world)]
+    ex.dist.all_gather(allc, counts, group=ex.group)
+    cnt = torch.stack(allc).cpu().numpy().reshape(-1)
+    longest = int(max(2 * cnt[2 * r] + cnt[2 * r + 1] for r in range(ex.world)))
+    n = lab_new.numel()
+    sparse = mode == "sparse" or (mode == "auto" and longest * 4 * ex.world < 5 * n)
+    if stats is not None:
+        stats["rounds"] += 1
+        stats["sparse_rounds"] += int(sparse)
+        b, e = ex.ranges[ex.rank]
+        stats["bytes"] += 4 * longest if sparse else 4 * (e - b) + n
+    if sparse:
+        stride = max(longest, 1)
+        with on_lib:
+            send = torch.zeros(stride, dtype=torch.int32, device=dev)
+            if lst is not None:
+                send[: lst.numel()].copy_(lst)
+            parts = [torch.empty(stride, dtype=torch.int32, device=dev) for _ in range(ex.world)]
+            ex.dist.all_gather(parts, send, group=ex.group)
+            recv = torch.cat(parts)
+        local = engine.part_det_apply(recv, stride, cnt, ex.world, ex.rank)
+        return ex.sum(local, dev)
+    engine.part_det_dense()
+    with on_lib:  # the exchange follows the round's kernels on the library stream
+        ex.labels(lab_new)
+        ex.flags(dirty)
+    return engine.part_det_import()  # global count (identical on every rank)
+
+
+def _det_sweep(engine, cfg, pickless, ex, lab_new, dirty, mode="auto", stats=None) -> int:
     """One deterministic partitioned sweep: speculative rounds until no rank
     holds a dirty vertex, then the commit.  Returns the
     rank-local count of changed owned vertices."""
@@ -157,16 +203,13 @@ def _det_sweep(engine, cfg, pickless, ex, lab_new, dirty) -> int:
     on_lib = _OnLibraryStream(engine, lab_new.device)
     while True:
         engine.part_det_round(cfg, pickless, rnd)  # kernels queued on the library stream
-        with on_lib:  # the exchange follows them on the same stream
-            ex.labels(lab_new)
-            ex.flags(dirty)
-        if engine.part_det_import() == 0:  # global count (identical on every rank): the round's one sync
+        if _det_round_exchange(engine, ex, lab_new, dirty, on_lib, mode, stats) == 0:
             break
         rnd += 1
     return engine.part_det_commit(cfg)
 
 
-def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) -> PartitionedResult:
+def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None, exchange="auto") -> PartitionedResult:
     """lpa_run (lpa.py:262-308) over the ranks of `group`; `engine` holds this
     rank's rows (Engine.part_gen_rmat / part_upload).  worker_count > 0: the
     asynchronous partitioned sweep; worker_count == 0: the deterministic one
@@ -184,11 +227,12 @@ def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) ->
     if det:
         lab_new, dirty = engine.part_det_buffers()
     history = []
+    stats = {"rounds": 0, "sparse_rounds": 0, "bytes": 0}
     converged = False
     for it in range(cfg.max_iterations):
         pickless = (it % cfg.pickless_gap) == 0
         if det:
-            local = _det_sweep(engine, cfg, pickless, ex, lab_new, dirty)
+            local = _det_sweep(engine, cfg, pickless, ex, lab_new, dirty, exchange, stats)
         else:
             local = engine.part_sweep(cfg, pickless)
         with on_lib:
@@ -203,7 +247,7 @@ def lpa_run_partitioned(engine, cfg, ranges, group=None, iteration_hook=None) ->
         if not pickless and (delta / n if n else 0.0) < cfg.tolerance:
             converged = True
             break
-    return PartitionedResult(len(history), history, converged)
+    return PartitionedResult(len(history), history, converged, stats["rounds"], stats["sparse_rounds"], stats["bytes"])
 
 
 def modularity_partitioned(engine, ranges, group=None) -> float:

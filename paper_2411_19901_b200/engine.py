@@ -331,6 +331,29 @@ class Engine:
         check(self.lib, self.ctx, self.lib.slpa_part_det_round(self.ctx, ctypes.byref(c), 1 if pickless else 0,
                                                                int(rnd)))
 
+    def part_det_collect(self):
+        """Sparse round exchange: (device int32 list, moved owned words, remote marks); the list holds
+        2 * words ints of (id, word) pairs followed by the mark ids."""
+        p, w, m = ctypes.c_uint64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib, self.ctx, self.lib.slpa_part_det_collect(self.ctx, ctypes.byref(p), ctypes.byref(w),
+                                                                 ctypes.byref(m)))
+        ln = 2 * w.value + m.value
+        lst = device_tensor(p.value, ln, "<i4", self.device) if ln else None
+        return lst, w.value, m.value
+
+    def part_det_apply(self, recv, stride, counts, world, rank) -> int:
+        """Apply the all-gathered lists (recv: device int32, rank r at r * stride); returns this rank's
+        dirty-vertex count."""
+        c = np.ascontiguousarray(counts, dtype=np.int64)
+        d = ctypes.c_int64()
+        ptr = recv.data_ptr() if recv is not None else 0
+        check(self.lib, self.ctx, self.lib.slpa_part_det_apply(self.ctx, ptr, int(stride), c.ctypes.data, int(world),
+                                                               int(rank), ctypes.byref(d)))
+        return d.value
+
+    def part_det_dense(self):
+        check(self.lib, self.ctx, self.lib.slpa_part_det_dense(self.ctx))
+
     def part_det_import(self) -> int:
         t = ctypes.c_int64(0)
         check(self.lib, self.ctx, self.lib.slpa_part_det_import(self.ctx, ctypes.byref(t)))

@@ -197,11 +197,48 @@ class MockDetEngine(MockEngine):
         import torch
         super().part_begin(cfg)
         self.lab_new = torch.arange(self.n, dtype=torch.int32)
+        self.lab_sent = np.arange(self.n, dtype=np.uint32)
         self.dirty = torch.zeros(self.n, dtype=torch.uint8)
         self.fnext = np.zeros(self.n, dtype=np.uint8)
 
     def part_det_buffers(self):
         return self.lab_new, self.dirty
+
+    # sparse round exchange (libslpa_b200 slpa_part_det_collect / _apply / _dense)
+    def part_det_collect(self):
+        import torch
+        L1 = self.lab_new.numpy().view(np.uint32)
+        d = self.dirty.numpy()
+        own = np.arange(self.v_begin, self.v_end)
+        moved = own[L1[own] != self.lab_sent[own]]
+        self.lab_sent[moved] = L1[moved]
+        mask = np.ones(self.n, dtype=bool)
+        mask[self.v_begin:self.v_end] = False
+        marks = np.flatnonzero((d != 0) & mask)
+        words = np.stack([moved.astype(np.int64), L1[moved].astype(np.int64)], axis=1).reshape(-1)
+        lst = np.concatenate([words, marks]).astype(np.uint32).view(np.int32)
+        return (torch.from_numpy(lst.copy()) if lst.size else None), int(moved.size), int(marks.size)
+
+    def part_det_apply(self, recv, stride, counts, world, rank):
+        L1 = self.lab_new.numpy().view(np.uint32)
+        d = self.dirty.numpy()
+        d[: self.v_begin] = 0
+        d[self.v_end:] = 0
+        r_all = recv.numpy()
+        for r in range(world):
+            if r == rank:
+                continue
+            nw, nm = int(counts[2 * r]), int(counts[2 * r + 1])
+            lst = r_all[r * stride: r * stride + 2 * nw + nm]
+            ids = lst[0:2 * nw:2]
+            L1[ids] = lst[1:2 * nw:2].view(np.uint32)
+            t = lst[2 * nw:]
+            t = t[(t >= self.v_begin) & (t < self.v_end)]
+            d[t] = 1
+        return int(d[self.v_begin:self.v_end].astype(np.int64).sum())
+
+    def part_det_dense(self):
+        pass
 
     def part_arc_hash(self):
         """Additive forward / reverse arc sums of the owned rows (the
@@ -261,6 +298,7 @@ class MockDetEngine(MockEngine):
         moved = (L1 & CHG) != 0
         L0[moved] = (L1[moved] & LMASK).astype(np.int32)
         L1[moved] &= LMASK
+        self.lab_sent[:] = L1
         self.fl.numpy()[:] = self.fnext
         return delta
 
@@ -277,13 +315,14 @@ def _det_worker(rank, world, port, payload, out):
     cfg = LpaConfig(**payload["cfg"])
     ranges = payload["ranges"]
     eng = MockDetEngine(g, ranges[rank][0], ranges[rank][1], get_oracle())
-    res = lpa_run_partitioned(eng, cfg, ranges)
+    res = lpa_run_partitioned(eng, cfg, ranges, exchange=payload.get("exchange", "auto"))
     out[rank] = (eng.lab.numpy().copy(), res.delta_history, res.converged)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("variant,world", [("mg", 2), ("bm", 2), ("mg", 3)])
-def test_gloo_deterministic_partition_equals_sequential_reference(oracle, variant, world):
+@pytest.mark.parametrize("variant,world,exchange", [("mg", 2, "auto"), ("bm", 2, "sparse"), ("mg", 3, "sparse"),
+                                                     ("mg", 3, "dense")])
+def test_gloo_deterministic_partition_equals_sequential_reference(oracle, variant, world, exchange):
     """The deterministic partitioned protocol reproduces the sequential sweep
     (the oracle, pinned to the reference's golden vectors) bit for bit."""
     import torch.multiprocessing as mp
@@ -292,7 +331,8 @@ def test_gloo_deterministic_partition_equals_sequential_reference(oracle, varian
     g = oracle.rmat(8, seed=33, permute=True)
     cfg = LpaConfig(variant=variant, degree_threshold=16, partial_groups=4)
     ranges = partition_ranges(g.num_vertices, world, np.diff(g.offsets))
-    payload = {"graph": (g.offsets, g.targets, g.weights), "cfg": cfg.__dict__, "ranges": ranges}
+    payload = {"graph": (g.offsets, g.targets, g.weights), "cfg": cfg.__dict__, "ranges": ranges,
+               "exchange": exchange}
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_det_worker, args=(world, _free_port(), payload, out), nprocs=world, join=True)
@@ -304,7 +344,7 @@ def test_gloo_deterministic_partition_equals_sequential_reference(oracle, varian
         np.testing.assert_array_equal(lab, ref.labels)
 
 
-def _gpu_det_worker(rank, world, port, scale, variant, out):
+def _gpu_det_worker(rank, world, port, scale, variant, out, exchange="auto"):
     import torch.distributed as dist
     import paper_2411_19901_b200 as slpa
     from paper_2411_19901_b200.distributed import lpa_run_partitioned, partition_ranges
@@ -315,15 +355,16 @@ def _gpu_det_worker(rank, world, port, scale, variant, out):
     ranges = eng.rmat_cuts(scale, world, seed=78, permute=True)  # arc-balanced
     eng.part_gen_rmat(scale, *ranges[rank], seed=78, permute=True)
     cfg = slpa.LpaConfig(variant=variant)
-    res = lpa_run_partitioned(eng, cfg, ranges)
+    res = lpa_run_partitioned(eng, cfg, ranges, exchange=exchange)
     lab, _ = eng.part_buffers()
     out[rank] = (lab.cpu().numpy(), res.delta_history, res.converged, res.iterations)
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant,world", [("mg", 2), ("bm", 2), ("mg", 3)])
-def test_gpu_deterministic_partition_bit_exact(oracle, variant, world):
+@pytest.mark.parametrize("variant,world,exchange", [("mg", 2, "auto"), ("bm", 2, "auto"), ("mg", 3, "auto"),
+                                                     ("mg", 2, "sparse"), ("mg", 3, "dense")])
+def test_gpu_deterministic_partition_bit_exact(oracle, variant, world, exchange):
     """Two / three processes share one B200 (gloo over CUDA tensors) and run
     the CUDA deterministic partitioned sweep: every replica equals the
     sequential reference (oracle) bit for bit."""
@@ -332,7 +373,7 @@ def test_gpu_deterministic_partition_bit_exact(oracle, variant, world):
     scale = 14
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_gpu_det_worker, args=(world, _free_port(), scale, variant, out), nprocs=world, join=True)
+    mp.spawn(_gpu_det_worker, args=(world, _free_port(), scale, variant, out, exchange), nprocs=world, join=True)
     g = oracle.rmat(scale, seed=78, permute=True)
     ref = oracle.lpa_run(g, LpaConfig(variant=variant))
     for r in range(world):
