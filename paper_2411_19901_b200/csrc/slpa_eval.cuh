@@ -263,10 +263,15 @@ __device__ __forceinline__ void lane_stream_u(const SweepArgs &a, int64_t start,
     }
     for (int64_t x0 = 0;;) {
         uint32_t L[kBatch];
+        if (DET && a.ident) {  // round 0 of the first sweep: a neighbour's label is its id (one branch per batch)
 #pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            L[j] = 0;
-            if (t[j] != v) L[j] = a.ident ? (uint32_t)t[j] : gather_word<DET>(a, t[j], v);
+            for (int j = 0; j < kBatch; ++j) L[j] = t[j] != v ? (uint32_t)t[j] : 0u;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                L[j] = 0;
+                if (t[j] != v) L[j] = gather_word<DET>(a, t[j], v);
+            }
         }
         const int64_t nx = x0 + kBatch;
         int32_t tn[kBatch];
@@ -387,15 +392,19 @@ __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, i
             const bool valid = in && t[j] != v;
             inr |= (unsigned)in << j;
             ok |= (unsigned)valid << j;
-            L[j] = 0;
-            if (valid)
-                L[j] = a.ident ? (uint32_t)t[j]
-                               : (DET && !a.lo_direct ? __ldcg(&a.lab_new[t[j]]) : gather_word<DET>(a, t[j], v));
         }
-        if (DET && !a.lo_direct && !a.ident) {  // lab_new-first: a changed higher neighbour's L0
+        if (DET && a.ident) {  // round 0 of the first sweep: a neighbour's label is its id (one branch per batch)
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) L[j] = ((ok >> j) & 1u) ? (uint32_t)t[j] : 0u;
+        } else if (DET && !a.lo_direct) {  // lab_new first, a changed higher neighbour's L0 after
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) L[j] = ((ok >> j) & 1u) ? __ldcg(&a.lab_new[t[j]]) : 0u;
 #pragma unroll
             for (int j = 0; j < kBatch; ++j)
                 if (((ok >> j) & 1u) && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) L[j] = ((ok >> j) & 1u) ? gather_word<DET>(a, t[j], v) : 0u;
         }
         const int64_t nb = b + kBatch;
         int32_t tn[kBatch];
@@ -772,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((unsigned)(b1 - b0)) : "memory");
     }
     const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
-    MgSketchDev<8, V> part;
+    MgSketchOff8 part;
     part.reset(8, a.zkey);
     int64_t cs = 0, ce = 0;
     if (lane < a.parts) chunk_bounds(hi - lo, a.parts, lane, cs, ce);
@@ -806,7 +815,7 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_merge(SweepArgs a, const int
     const uint2 meta = __ldcg(&a.hmeta[idx]);
     if (!(meta.y & 1u)) return;
     const uint32_t *src = a.hparts + (size_t)idx * kLpmWords;
-    MgSketchDev<8, V> S;
+    MgSketchOff8 S;
     S.reset(8, a.zkey);
     uint32_t kk[8], vv[8], kn[8], vn[8];
     ld8(src, kk);

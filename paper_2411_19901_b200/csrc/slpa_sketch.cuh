@@ -192,8 +192,7 @@ struct MgSketchDev {
 // "first slot with value 0" (sketch.py:66-70).  One accumulate is ~60
 // predicated instructions and no branches, so the lanes of a warp never
 // diverge on hit / insert / decrement.
-template <>
-struct MgSketchDev<8, uint32_t> {
+struct MgSketchOff8 {
     int32_t key[8];
     uint32_t s[8];
     uint32_t D;
@@ -293,6 +292,11 @@ struct MgSketchDev<8, uint32_t> {
         return found;
     }
 };
+
+// Every k = 8, integer-value sketch is the offset form (MgSketchDev<8, uint32_t>
+// derives from it): the light, heavy and giant kernels all use it.
+template <>
+struct MgSketchDev<8, uint32_t> : MgSketchOff8 {};
 
 // BmState (sketch.py:140-162)
 template <class V = double>
