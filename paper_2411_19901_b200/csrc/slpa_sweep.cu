@@ -348,7 +348,7 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     a.zkey = ctx->zkey;
     static const int lo_direct = [] {
         const char *e = getenv("SLPA_LO_DIRECT");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 1;
     }();
     a.lo_direct = lo_direct;
     static const int pf = [] {
