@@ -353,7 +353,7 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     a.lo_direct = lo_direct;
     static const int pf = [] {
         const char *e = getenv("SLPA_HI_PREFETCH");
-        return e ? atoi(e) : 1;
+        return e ? atoi(e) : 0;
     }();
     a.pf = pf;
     a.giant_bin = g.bin_giant.p;

@@ -60,6 +60,7 @@ ENVS = [
     {"SLPA_DEFER_MIN": "0", "SLPA_GIANT": "300"},
     {"SLPA_DEFER_MIN": "50", "SLPA_GIANT": "300"},
     {"SLPA_GIANT_ASYNC": "0", "SLPA_GIANT": "300"},
+    {"SLPA_ASYNC_SPLIT": "0", "SLPA_GIANT": "300"},
     {"SLPA_HI_SMALL": "0", "SLPA_GIANT": "300"},
     {"SLPA_HI_SMALL": "100000000"},
     {"SLPA_LO_SMALL": "0"},
