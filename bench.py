@@ -267,7 +267,7 @@ def workload_config(args, n, m, world):
         "vertices": n, "arcs": m, "variant": args.variant,
         "mode": "deterministic (bit-exact sequential)" if args.mode == "det" else "async",
         "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
-        "l2_policy": "inputs larger than L2 (CSR ~4.3 GB >> 126 MB L2)",
+        "l2_policy": f"inputs larger than L2 (CSR ~{(8 * (n + 1) + 8 * m) / 1e9:.1f} GB >> 126 MB L2)",
     }
 
 

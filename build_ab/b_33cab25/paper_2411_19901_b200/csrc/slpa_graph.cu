@@ -963,87 +963,11 @@ static void assemble_from_keys(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &keys,
 static int key_end_bit(int64_t n) { return 32 + ceil_log2((uint64_t)(n > 1 ? n : 2)) + 1; }
 static uint64_t drop_key(int64_t n) { return 1ULL << (key_end_bit(n) - 1); }
 
-void slpa_part_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
-                             uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t r0,
-                             int64_t r1);
-
-namespace {
-__global__ void k_shift_range_offsets(const int64_t *__restrict__ src, int64_t r0, int64_t r1, int64_t add,
-                                      int64_t *__restrict__ dst) {
-    const int64_t v = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < r1) dst[v] = src[v] + add;
-}
-}  // namespace
-
-// Large graphs (SURVEY C5 on one GPU: 2^31 edges): one-shot assembly would
-// sort 2^31 keys and then 2^32 arcs.  Instead the rows are built range by
-// range -- for each of R contiguous vertex ranges the partitioned generator
-// keeps the edges touching the range and assembles its rows -- and the
-// ranges' arcs are appended into one CSR (sorted rows, the same graph).
-static int64_t gen_ranges_for(int64_t num_edges) {
-    static const int64_t forced = [] {
-        const char *e = getenv("SLPA_GEN_RANGES");
-        return e ? atoll(e) : 0LL;
-    }();
-    if (forced > 0) return forced;
-    return num_edges > (1LL << 29) ? (num_edges + (1LL << 28) - 1) >> 28 : 1;
-}
-
-static void gen_rmat_ranged(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
-                            uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t R) {
-    const int64_t n = 1LL << scale;
-    cudaStream_t s = ctx->stream;
-    DeviceGraph &g = ctx->g;
-    const int64_t cap = 2 * num_edges;  // arcs: at most both directions of every edge
-    DevBuf<int64_t> off;
-    DevBuf<int32_t> tgt;
-    DevBuf<float> w;
-    off.alloc(n + 1);
-    tgt.alloc(cap);
-    w.alloc(cap);
-    int64_t M = 0;
-    for (int64_t r = 0; r < R; ++r) {
-        const int64_t r0 = n * r / R, r1 = n * (r + 1) / R;
-        slpa_part_gen_rmat_impl(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key, r0, r1);
-        const int64_t mloc = g.base.m;
-        SLPA_REQUIRE(M + mloc <= cap, SLPA_ECUDA, "ranged generator overflow");
-        if (r1 > r0)
-            k_shift_range_offsets<<<grid_for(r1 - r0, kT), kT, 0, s>>>(g.base.off.p, r0, r1, M, off.p);
-        if (mloc) {
-            CUDA_TRY(cudaMemcpyAsync(tgt.p + M, g.base.tgt.p, mloc * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(w.p + M, g.base.w32.p, mloc * sizeof(float), cudaMemcpyDeviceToDevice, s));
-        }
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaStreamSynchronize(s));
-        M += mloc;
-    }
-    CUDA_TRY(cudaMemcpyAsync(off.p + n, &M, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    g.base.release();
-    g.base.n = n;
-    g.base.m = M;
-    g.base.off = std::move(off);
-    g.base.tgt = std::move(tgt);
-    g.base.w32 = std::move(w);
-    g.n = n;
-    g.m = M;
-    g.w_f64 = 0;
-    g.perm.release();
-    g.ids.release();
-    g.pos.release();
-    g.has_order = 0;
-}
-
 void slpa_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
                         uint64_t seed, int32_t permute, uint64_t perm_key) {
     SLPA_REQUIRE(scale >= 1 && scale <= 31, SLPA_EINVAL, "rmat scale must be in [1, 31]");
     SLPA_REQUIRE(num_edges >= 0, SLPA_EINVAL, "num_edges must be non-negative");
     const int64_t n = 1LL << scale;
-    const int64_t R = gen_ranges_for(num_edges);
-    if (R > 1) {
-        gen_rmat_ranged(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key, R);
-        return;
-    }
     DevBuf<uint64_t> keys;
     keys.alloc(num_edges);
     if (num_edges > 0)

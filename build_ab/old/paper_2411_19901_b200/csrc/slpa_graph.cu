@@ -458,11 +458,9 @@ __device__ __forceinline__ int64_t row_of(const int64_t *off, int64_t lo, int64_
 template <class W>
 __global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const int32_t *tgt, const W *w, int64_t n,
                                                     int64_t m, unsigned long long *acc, unsigned *bad,
-                                                    unsigned long long *wmax, unsigned long long *dmax,
-                                                    int64_t e_begin = 0) {
-    // arcs [e_begin, m) -- the whole graph, or one chunk of a pipelined upload
+                                                    unsigned long long *wmax, unsigned long long *dmax) {
     __shared__ int64_t s_r[2];
-    const int64_t e0 = e_begin + (int64_t)blockIdx.x * kArcBlock;
+    const int64_t e0 = (int64_t)blockIdx.x * kArcBlock;
     if (e0 >= m) return;
     const int64_t e1 = min(m, e0 + kArcBlock);
     if (threadIdx.x == 0) {
@@ -481,7 +479,7 @@ __global__ void __launch_bounds__(256) k_arc_checks(const int64_t *off, const in
         for (int j = 0; j < kArcPer; ++j) {
             const int64_t e = a0 + j;
             if (e >= e1) break;
-            while (e >= next && u < n - 1) {  // (bounded: offsets are validated concurrently)
+            while (e >= next) {
                 ++u;
                 start = next;
                 next = __ldg(&off[u + 1]);
@@ -549,46 +547,6 @@ void slpa_arc_hash_impl(slpa_ctx *ctx, uint64_t out[4]) {
     for (int i = 0; i < 4; ++i) out[i] = h[i];
 }
 
-// k_arc_checks over arcs [e0, e1) of `c` into acc[0..7] (stream order).
-void slpa_arc_checks_range(slpa_ctx *ctx, const Csr &c, int w_f64, int64_t e0, int64_t e1, unsigned long long *acc) {
-    if (e1 <= e0) return;
-    const unsigned blocks = (unsigned)((e1 - e0 + kArcBlock - 1) / kArcBlock);
-    cudaStream_t s = ctx->stream;
-    if (w_f64)
-        k_arc_checks<double><<<blocks, 256, 0, s>>>(c.off.p, c.tgt.p, c.w64.p, c.n, e1, acc, (unsigned *)(acc + 4),
-                                                      acc + 5, acc + 6, e0);
-    else
-        k_arc_checks<float><<<blocks, 256, 0, s>>>(c.off.p, c.tgt.p, c.w32.p, c.n, e1, acc, (unsigned *)(acc + 4),
-                                                     acc + 5, acc + 6, e0);
-    CUDA_TRY(cudaGetLastError());
-}
-
-// k_validate_arcs over arcs [e0, e1) (stream order; flags into err).
-void slpa_validate_arcs_range(slpa_ctx *ctx, const Csr &c, int w_f64, int64_t e0, int64_t e1, unsigned *err) {
-    if (e1 <= e0) return;
-    if (w_f64)
-        k_validate_arcs<double><<<grid_for(e1 - e0, kT), kT, 0, ctx->stream>>>(c.tgt.p + e0, c.w64.p + e0, c.n,
-                                                                                e1 - e0, err);
-    else
-        k_validate_arcs<float><<<grid_for(e1 - e0, kT), kT, 0, ctx->stream>>>(c.tgt.p + e0, c.w32.p + e0, c.n,
-                                                                               e1 - e0, err);
-    CUDA_TRY(cudaGetLastError());
-}
-
-// Offsets check of a freshly copied CSR (flags into err; stream order).
-void slpa_validate_offsets_async(slpa_ctx *ctx, const Csr &c, unsigned *err) {
-    k_validate_offsets<<<grid_for(c.n + 1, kT), kT, 0, ctx->stream>>>(c.off.p, c.n, c.m, err);
-    CUDA_TRY(cudaGetLastError());
-}
-
-void slpa_throw_validation(unsigned e) {
-    if (e & 1) throw SlpaError{SLPA_EINVAL, "offsets must be a 1-d array starting at 0"};
-    if (e & 2) throw SlpaError{SLPA_EINVAL, "offsets must be non-decreasing"};
-    if (e & 4) throw SlpaError{SLPA_EINVAL, "offsets[-1] must equal the arc count"};
-    if (e & 8) throw SlpaError{SLPA_EINVAL, "arc target out of range"};
-    if (e & 16) throw SlpaError{SLPA_EINVAL, "arc weights must be positive"};
-}
-
 // Symmetry check + reverse CSR of the active numbering; resets the bins.
 void slpa_graph_finalize(slpa_ctx *ctx) {
     DeviceGraph &g = ctx->g;
@@ -601,22 +559,23 @@ void slpa_graph_finalize(slpa_ctx *ctx) {
     g.rsrc.release();
     g.symmetric = 1;
     g.int_weights = 1;
-    const bool pre = ctx->pre_checks_valid;
-    ctx->pre_checks_valid = 0;
     if (g.n == 0 || g.m == 0) return;
-    // acc: 4 hashes, bad flag, max weight, max degree (one readback); a
-    // pipelined upload computed them while the arcs were copied
+    // acc: 4 hashes, bad flag, max weight, max degree (one readback)
+    DevBuf<unsigned long long> acc;
+    acc.alloc(8);
+    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 8 * sizeof(unsigned long long), s));
+    const unsigned blocks = (unsigned)((g.m + kArcBlock - 1) / kArcBlock);
+    if (g.w_f64)
+        k_arc_checks<double><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const double *)g.w(), g.n, g.m, acc.p,
+                                                      (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
+    else
+        k_arc_checks<float><<<blocks, 256, 0, s>>>(g.off(), g.tgt(), (const float *)g.w(), g.n, g.m, acc.p,
+                                                     (unsigned *)(acc.p + 4), acc.p + 5, acc.p + 6);
+    CUDA_TRY(cudaGetLastError());
     unsigned long long h[8];
-    if (pre) {
-        for (int i = 0; i < 8; ++i) h[i] = ctx->pre_checks[i];
-    } else {
-        DevBuf<unsigned long long> acc;
-        acc.alloc(8);
-        CUDA_TRY(cudaMemsetAsync(acc.p, 0, 8 * sizeof(unsigned long long), s));
-        slpa_arc_checks_range(ctx, g.act(), g.w_f64, 0, g.m, acc.p);
-        CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-    }
+    CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    acc.release();
     g.symmetric = (h[0] == h[1]) && (h[2] == h[3]);
     g.max_deg = (int64_t)h[6];
     // integer sketch values need integral weights and every weighted degree
@@ -656,7 +615,6 @@ void slpa_graph_apply_order(slpa_ctx *ctx, const int64_t *order, bool on_device)
         slpa_graph_finalize(ctx);
         return;
     }
-    ctx->pre_checks_valid = 0;  // the checks run on the permuted CSR (the reverse CSR must be built in it)
     const int64_t n = g.n, m = g.m;
     DevBuf<int64_t> d_order;
     const int64_t *ord = order;
@@ -963,87 +921,11 @@ static void assemble_from_keys(slpa_ctx *ctx, int64_t n, DevBuf<uint64_t> &keys,
 static int key_end_bit(int64_t n) { return 32 + ceil_log2((uint64_t)(n > 1 ? n : 2)) + 1; }
 static uint64_t drop_key(int64_t n) { return 1ULL << (key_end_bit(n) - 1); }
 
-void slpa_part_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
-                             uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t r0,
-                             int64_t r1);
-
-namespace {
-__global__ void k_shift_range_offsets(const int64_t *__restrict__ src, int64_t r0, int64_t r1, int64_t add,
-                                      int64_t *__restrict__ dst) {
-    const int64_t v = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < r1) dst[v] = src[v] + add;
-}
-}  // namespace
-
-// Large graphs (SURVEY C5 on one GPU: 2^31 edges): one-shot assembly would
-// sort 2^31 keys and then 2^32 arcs.  Instead the rows are built range by
-// range -- for each of R contiguous vertex ranges the partitioned generator
-// keeps the edges touching the range and assembles its rows -- and the
-// ranges' arcs are appended into one CSR (sorted rows, the same graph).
-static int64_t gen_ranges_for(int64_t num_edges) {
-    static const int64_t forced = [] {
-        const char *e = getenv("SLPA_GEN_RANGES");
-        return e ? atoll(e) : 0LL;
-    }();
-    if (forced > 0) return forced;
-    return num_edges > (1LL << 29) ? (num_edges + (1LL << 28) - 1) >> 28 : 1;
-}
-
-static void gen_rmat_ranged(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB,
-                            uint32_t tABC, uint64_t seed, int32_t permute, uint64_t perm_key, int64_t R) {
-    const int64_t n = 1LL << scale;
-    cudaStream_t s = ctx->stream;
-    DeviceGraph &g = ctx->g;
-    const int64_t cap = 2 * num_edges;  // arcs: at most both directions of every edge
-    DevBuf<int64_t> off;
-    DevBuf<int32_t> tgt;
-    DevBuf<float> w;
-    off.alloc(n + 1);
-    tgt.alloc(cap);
-    w.alloc(cap);
-    int64_t M = 0;
-    for (int64_t r = 0; r < R; ++r) {
-        const int64_t r0 = n * r / R, r1 = n * (r + 1) / R;
-        slpa_part_gen_rmat_impl(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key, r0, r1);
-        const int64_t mloc = g.base.m;
-        SLPA_REQUIRE(M + mloc <= cap, SLPA_ECUDA, "ranged generator overflow");
-        if (r1 > r0)
-            k_shift_range_offsets<<<grid_for(r1 - r0, kT), kT, 0, s>>>(g.base.off.p, r0, r1, M, off.p);
-        if (mloc) {
-            CUDA_TRY(cudaMemcpyAsync(tgt.p + M, g.base.tgt.p, mloc * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(w.p + M, g.base.w32.p, mloc * sizeof(float), cudaMemcpyDeviceToDevice, s));
-        }
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaStreamSynchronize(s));
-        M += mloc;
-    }
-    CUDA_TRY(cudaMemcpyAsync(off.p + n, &M, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    g.base.release();
-    g.base.n = n;
-    g.base.m = M;
-    g.base.off = std::move(off);
-    g.base.tgt = std::move(tgt);
-    g.base.w32 = std::move(w);
-    g.n = n;
-    g.m = M;
-    g.w_f64 = 0;
-    g.perm.release();
-    g.ids.release();
-    g.pos.release();
-    g.has_order = 0;
-}
-
 void slpa_gen_rmat_impl(slpa_ctx *ctx, int32_t scale, int64_t num_edges, uint32_t tA, uint32_t tAB, uint32_t tABC,
                         uint64_t seed, int32_t permute, uint64_t perm_key) {
     SLPA_REQUIRE(scale >= 1 && scale <= 31, SLPA_EINVAL, "rmat scale must be in [1, 31]");
     SLPA_REQUIRE(num_edges >= 0, SLPA_EINVAL, "num_edges must be non-negative");
     const int64_t n = 1LL << scale;
-    const int64_t R = gen_ranges_for(num_edges);
-    if (R > 1) {
-        gen_rmat_ranged(ctx, scale, num_edges, tA, tAB, tABC, seed, permute, perm_key, R);
-        return;
-    }
     DevBuf<uint64_t> keys;
     keys.alloc(num_edges);
     if (num_edges > 0)
