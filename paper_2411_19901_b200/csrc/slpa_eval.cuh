@@ -7,9 +7,6 @@
 #include "slpa_internal.cuh"
 
 // minimum resident blocks per SM for the two bulk kernels (register caps; A/B builds)
-#ifndef SLPA_HI_EF
-#define SLPA_HI_EF 0
-#endif
 #ifndef SLPA_HI_MINB
 #define SLPA_HI_MINB 1
 #endif
@@ -65,22 +62,6 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t *ptr, uint64_t pol) {
 __device__ __forceinline__ float ld_stream(const float *ptr, uint64_t pol) {
     float r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-// L1-allocating flavour (a lane's consecutive scalar loads share sectors)
-__device__ __forceinline__ int32_t ld_stream_l1(const int32_t *ptr, uint64_t pol) {
-    int32_t r;
-    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ float ld_stream_l1(const float *ptr, uint64_t pol) {
-    float r;
-    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ double ld_stream_l1(const double *ptr, uint64_t pol) {
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
     return r;
 }
 __device__ __forceinline__ double ld_stream(const double *ptr, uint64_t pol) {
@@ -325,22 +306,12 @@ __device__ __forceinline__ void lane_stream_u(const SweepArgs &a, int64_t start,
 template <class W, bool DET>
 __device__ __forceinline__ void ld_batch_u(const SweepArgs &a, const W *__restrict__ wts, int64_t start, int64_t x,
                                            int64_t len, int32_t v, int32_t (&t)[kBatch], W (&w)[kBatch]) {
-#if SLPA_HI_EF
-    const uint64_t pol = policy_evict_first();
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-        const bool in = x + j < len;
-        t[j] = in ? ld_stream_l1(&a.tgt[start + x + j], pol) : v;
-        w[j] = in ? ld_stream_l1(&wts[start + x + j], pol) : (W)0;
-    }
-#else
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
         const bool in = x + j < len;
         t[j] = in ? __ldg(&a.tgt[start + x + j]) : v;
         w[j] = in ? __ldg(&wts[start + x + j]) : (W)0;
     }
-#endif
 }
 
 // The high-degree scans gather every word from lab_new, the array L2 keeps
