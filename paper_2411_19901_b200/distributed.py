@@ -7,7 +7,8 @@ SURVEY §8(e2)), per sweep:
 
 1. every rank sweeps its own rows in place (libslpa_b200 ``slpa_part_sweep``)
    reading its label replica -- remote labels are one exchange old;
-2. the owned label ranges are all-gathered into every replica;
+2. each owned label range is broadcast from its owner into every replica,
+   in place;
 3. the flag arrays are max-reduced: a rank's remote entries carry the
    "neighbour changed" marks of lpa.py:223 for vertices other ranks own;
    ``slpa_part_end_exchange`` then clears the remote entries;
@@ -18,8 +19,8 @@ rounds of the single-GPU engine across ranks: per round every
 rank evaluates its owned flagged / dirty vertices, then publishes the owned
 speculative label words (lab_new, bit 31 = changed) that moved and the dirty
 marks it set on other ranks' vertices -- as changed-only lists when they are
-short (most rounds), else densely (the owned ranges all-gathered, the marks
-MAX-reduced as bytes); the sweep ends when no mark is set anywhere.  Stale remote reads are re-evaluated through the marks like any
+short (most rounds), else densely (the owned ranges broadcast in place, the
+marks MAX-reduced as bytes); the sweep ends when no mark is set anywhere.  Stale remote reads are re-evaluated through the marks like any
 other speculation, so labels, delta history and iteration count are
 bit-identical to the sequential reference (lpa.py:204-224).
 
@@ -54,7 +55,7 @@ def partition_ranges(n: int, world: int, degrees=None):
 
 
 class Exchange:
-    """Label all-gather + flag max-reduction over torch.distributed."""
+    """Label exchange + flag max-reduction over torch.distributed."""
 
     def __init__(self, ranges, group=None):
         import torch.distributed as dist
@@ -63,21 +64,15 @@ class Exchange:
         self.ranges = ranges
         self.world = len(ranges)
         self.rank = dist.get_rank(group)
-        self.maxlen = max(max(e - b for b, e in ranges), 1)
-        self._send = None
-        self._recv = None
 
     def labels(self, lab):
-        import torch
-        if self._send is None or self._send.device != lab.device:
-            self._send = torch.zeros(self.maxlen, dtype=lab.dtype, device=lab.device)
-            self._recv = [torch.zeros(self.maxlen, dtype=lab.dtype, device=lab.device) for _ in range(self.world)]
-        b, e = self.ranges[self.rank]
-        self._send[: e - b].copy_(lab[b:e])
-        self.dist.all_gather(self._recv, self._send, group=self.group)
+        """Every rank's owned range of `lab` into every replica, in place: one
+        broadcast per rank from the owner, straight out of and into the label
+        array (no staging copies; the ranges need not be equal)."""
         for r, (rb, re) in enumerate(self.ranges):
-            if r != self.rank and re > rb:
-                lab[rb:re].copy_(self._recv[r][: re - rb])
+            if re > rb:
+                src = r if self.group is None else self.dist.get_global_rank(self.group, r)
+                self.dist.broadcast(lab[rb:re], src=src, group=self.group)
 
     def flags(self, fl):
         self.dist.all_reduce(fl, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -159,7 +154,7 @@ def _det_round_exchange(engine, ex, lab_new, dirty, on_lib, mode, stats=None) ->
     sparse: every rank publishes the owned label words that moved since its
     last exchange and the marks it set on remote vertices (one all-gather of
     padded int32 lists); dense: the owned ranges of the label words are
-    all-gathered and the dirty marks MAX-reduced as bytes.  "auto" picks the
+    broadcast in place and the dirty marks MAX-reduced as bytes.  "auto" picks the
     sparse exchange unless the longest list would move more bytes than the
     dense one -- decided from the all-gathered counts, so every rank agrees."""
     import torch

@@ -68,6 +68,7 @@ ENVS = [
     {"SLPA_COMMIT_POS": "0", "SLPA_SCAN_SORT_MIN": "0"},
     {"SLPA_LO_SMALL": "100000000", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "1000", "SLPA_HI_SPLIT": "300"},
+    {"SLPA_HI_SLICE": "1000", "SLPA_GIANT": "300"},
 ]
 
 
