@@ -231,17 +231,21 @@ __global__ void __launch_bounds__(kThreads) k_commit_lo(SweepArgs a, const int32
     warp_count(a.counters, 0, 0, d);
 }
 
-__global__ void __launch_bounds__(kThreads) k_commit_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count) {
+__global__ void __launch_bounds__(kThreads) k_commit_hi(SweepArgs a, const int32_t *__restrict__ list, int64_t count,
+                                                     bool marks = true) {
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= count) return;
     const int32_t v = __ldg(&list[wid]);
     uint32_t wv = a.lab_new[v];
     if (!(wv & SLPA_CHG)) return;
-    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-    for (int64_t e = lo + lane; e < hi; e += 32) {
-        int32_t t = __ldg(&a.tgt[e]);
-        if (t <= v) mark_flag(a, t);
+    if (marks) {
+        const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+#pragma unroll 4
+        for (int64_t e = lo + lane; e < hi; e += 32) {
+            int32_t t = __ldg(&a.tgt[e]);
+            if (t <= v) mark_flag(a, t);
+        }
     }
     __syncwarp();
     if (lane == 0) {
@@ -249,6 +253,25 @@ __global__ void __launch_bounds__(kThreads) k_commit_hi(SweepArgs a, const int32
         a.lab_old[v] = c;
         a.lab_new[v] = (uint32_t)c;
         ctr_add(a.counters, CNT_DELTA, 1ull);
+    }
+}
+
+// The giants' next-sweep marks: one warp walking a row of ~4e5 arcs is a
+// chain of dependent load rounds (measured 3.4 ms for sweep 1's commit at
+// RMAT s24), so the rows are cut into kCommitArcs slices, a block each
+// (blockIdx.y = giant).  k_commit_hi(marks = false) then commits the labels.
+constexpr int kCommitArcs = 4096;
+__global__ void __launch_bounds__(kThreads) k_commit_marks_wide(SweepArgs a, const int32_t *__restrict__ list) {
+    const int32_t v = __ldg(&list[blockIdx.y]);
+    if (!(__ldcg(&a.lab_new[v]) & SLPA_CHG)) return;
+    const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
+    const int64_t b = lo + (int64_t)blockIdx.x * kCommitArcs;
+    if (b >= hi) return;
+    const int64_t end = b + kCommitArcs < hi ? b + kCommitArcs : hi;
+#pragma unroll 4
+    for (int64_t e = b + threadIdx.x; e < end; e += kThreads) {
+        const int32_t t = __ldg(&a.tgt[e]);
+        if (t <= v) mark_flag(a, t);
     }
 }
 
@@ -549,6 +572,14 @@ int64_t hi_slice() {
         return e ? std::max<int64_t>(1, atoll(e)) : 262144LL;
     }();
     return m;
+}
+
+// Commit of the giant bin: wide marks, then the labels.
+void commit_giants(slpa_ctx *ctx, const SweepArgs &a, cudaStream_t s) {
+    const DeviceGraph &g = ctx->g;
+    const int64_t slices = std::max<int64_t>(1, (g.giant_max_deg + kCommitArcs - 1) / kCommitArcs);
+    k_commit_marks_wide<<<dim3((unsigned)slices, (unsigned)g.n_giant), kThreads, 0, s>>>(a, g.bin_giant.p);
+    k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant, false);
 }
 
 void launch_hi(slpa_ctx *ctx, const KernelSet &ks, const SweepArgs &a, const int32_t *list, int64_t cnt, int round0,
@@ -1069,8 +1100,7 @@ int64_t slpa_part_det_commit_impl(slpa_ctx *ctx, const slpa_config *cfg) {
     if (g.n_lo > 0) k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
     if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
     if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
-    if (g.n_giant > 0)
-        k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
+    if (g.n_giant > 0) commit_giants(ctx, a, s);
     if (n > 0) k_fold_all<<<grid_for(n, kThreads), kThreads, 0, s>>>(wb.lab_old.p, wb.lab_new.p, n);
     if (n > 0) k_flag_bits_to_bytes<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, s>>>(wb.fbits.p, wb.flag_a.p, n);
     if (n > 0)  // every rank folded the same words: the published state is the folded one
@@ -1289,15 +1319,14 @@ int64_t slpa_sweep_det(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     // commit: L0 <- L1, delta, next-sweep flags pushed from the changed rows
     const int64_t fwords = (n + 31) / 32;
     CUDA_TRY(cudaMemsetAsync(wb.fbits.p, 0, (size_t)fwords * sizeof(uint32_t), s));
-    timed_launch(ctx, SLPA_PROF_COMMIT, 5, [&] {
+    timed_launch(ctx, SLPA_PROF_COMMIT, g.n_giant > 0 ? 6 : 5, [&] {
         if (g.n_lo > 0) {
             if (commit_pos_mode()) k_commit_lo_pos<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, n);
             else k_commit_lo<<<grid_for(g.n_lo, kThreads), kThreads, 0, s>>>(a, g.bin_lo.p, g.n_lo);
         }
         if (g.n_mid > 0) k_commit_hi<<<grid_for(g.n_mid * 32, kThreads), kThreads, 0, s>>>(a, g.bin_mid.p, g.n_mid);
         if (g.n_hi > 0) k_commit_hi<<<grid_for(g.n_hi * 32, kThreads), kThreads, 0, s>>>(a, g.bin_hi.p, g.n_hi);
-        if (g.n_giant > 0)
-            k_commit_hi<<<grid_for(g.n_giant * 32, kThreads), kThreads, 0, s>>>(a, g.bin_giant.p, g.n_giant);
+        if (g.n_giant > 0) commit_giants(ctx, a, s);
         if (n > 0) k_flag_bits_to_bytes<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, s>>>(wb.fbits.p, wb.flag_b.p, n);
         CUDA_TRY(cudaGetLastError());
     });
