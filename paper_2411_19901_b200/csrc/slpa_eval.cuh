@@ -18,6 +18,12 @@
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef SLPA_GCS_DEPTH
+#define SLPA_GCS_DEPTH 8
+#endif
+#ifndef SLPA_GIANT_RING
+#define SLPA_GIANT_RING 4
+#endif
 constexpr int kGiantWarps = 8;  // block-per-vertex kernels: 8 warps x 4 groups = 32 chunks
 
 // ------------------------------------------------------------------ label reads
@@ -870,7 +876,7 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_finish(SweepArgs a, const in
 template <class W, bool DET, class V>
 __device__ __forceinline__ void group_chunk_scan(const SweepArgs &a, int64_t start, int64_t len, int64_t maxlen,
                                                  int32_t v, int sl, int gb, int32_t &key, V &val, bool &lc) {
-    constexpr int D = 4;  // batches in flight
+    constexpr int D = SLPA_GCS_DEPTH;  // batches in flight (each a target load -> label gather chain)
     const W *__restrict__ wts = reinterpret_cast<const W *>(a.w);
     uint32_t Lr[D];
     W wr[D];
@@ -1293,37 +1299,44 @@ __global__ void __launch_bounds__(kGiantWarps * 32) k_mg_giant_grp(SweepArgs a, 
     int32_t key = kNoKey;
     V val = (V)0;
     bool lc = false;
-    uint32_t Ln = 0;
-    W wn = (W)0;
-    if (sl < len) {
-        Ln = __ldcg(&a.glab[base + cs + sl]);
-        wn = __ldcg(&gw[base + cs + sl]);
-    }
-    for (int64_t x = 0; x < maxlen; x += 8) {
-        const uint32_t Lx = Ln;
-        const W wx = wn;
-        Ln = 0;
-        wn = (W)0;
-        if (x + 8 + sl < len) {  // next batch of the group requested ahead
-            Ln = __ldcg(&a.glab[base + cs + x + 8 + sl]);
-            wn = __ldcg(&gw[base + cs + x + 8 + sl]);
-        }
+    // ring of kGiantRing batches in flight per group: the chain consumes a
+    // batch (8 dependent accumulates) in far less than one memory latency
+    constexpr int kGiantRing = SLPA_GIANT_RING;
+    uint32_t Lr[kGiantRing];
+    W wr[kGiantRing];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t Lj = __shfl_sync(0xffffffffu, Lx, gb + j);
-            const W wj = __shfl_sync(0xffffffffu, wx, gb + j);
-            const bool live = x + j < len && wj != (W)0;  // group-uniform
-            lc |= live && (Lj >> 31) != 0;
-            const int32_t c = (int32_t)(Lj & SLPA_LMASK);
-            const V w = (V)wj;
-            const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c, a.zkey)) >> gb) & 0xffu;
-            const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
-            const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
-            const V d = (mm | fm) ? (V)0 : w;
-            if (live) {
-                const bool mine = (sel >> sl) & 1u;
-                if (mine) key = c;
-                val = mine ? val + w : val - (val < d ? val : d);
+    for (int d = 0; d < kGiantRing; ++d) {
+        const int64_t e = (int64_t)d * 8 + sl;
+        Lr[d] = e < len ? __ldcg(&a.glab[base + cs + e]) : 0u;
+        wr[d] = e < len ? __ldcg(&gw[base + cs + e]) : (W)0;
+    }
+    for (int64_t x0 = 0; x0 < maxlen; x0 += 8 * kGiantRing) {
+#pragma unroll
+        for (int d = 0; d < kGiantRing; ++d) {
+            const int64_t x = x0 + (int64_t)d * 8;
+            if (x >= maxlen) break;  // warp-uniform
+            const uint32_t Lx = Lr[d];
+            const W wx = wr[d];
+            const int64_t e = x + 8 * kGiantRing + sl;  // refill: the batch kGiantRing ahead
+            Lr[d] = e < len ? __ldcg(&a.glab[base + cs + e]) : 0u;
+            wr[d] = e < len ? __ldcg(&gw[base + cs + e]) : (W)0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t Lj = __shfl_sync(0xffffffffu, Lx, gb + j);
+                const W wj = __shfl_sync(0xffffffffu, wx, gb + j);
+                const bool live = x + j < len && wj != (W)0;  // group-uniform
+                lc |= live && (Lj >> 31) != 0;
+                const int32_t c = (int32_t)(Lj & SLPA_LMASK);
+                const V w = (V)wj;
+                const unsigned mm = (__ballot_sync(0xffffffffu, key_matches(key, c, a.zkey)) >> gb) & 0xffu;
+                const unsigned fm = (__ballot_sync(0xffffffffu, val == (V)0) >> gb) & 0xffu;
+                const unsigned sel = mm ? (mm & (0u - mm)) : (fm & (0u - fm));
+                const V dd = (mm | fm) ? (V)0 : w;
+                if (live) {
+                    const bool mine = (sel >> sl) & 1u;
+                    if (mine) key = c;
+                    val = mine ? val + w : val - (val < dd ? val : dd);
+                }
             }
         }
     }
