@@ -402,12 +402,6 @@ __device__ __forceinline__ void lane_stream(const SweepArgs &a, int64_t start, i
         if (DET && a.ident) {  // round 0 of the first sweep: a neighbour's label is its id (one branch per batch)
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) L[j] = ((ok >> j) & 1u) ? (uint32_t)t[j] : 0u;
-        } else if (DET && !a.lo_direct) {  // lab_new first, a changed higher neighbour's L0 after
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) L[j] = ((ok >> j) & 1u) ? __ldcg(&a.lab_new[t[j]]) : 0u;
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j)
-                if (((ok >> j) & 1u) && t[j] > v && (L[j] >> 31)) L[j] = (uint32_t)__ldg(&a.lab_old[t[j]]);
         } else {
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) L[j] = ((ok >> j) & 1u) ? gather_word<DET>(a, t[j], v) : 0u;
@@ -779,27 +773,15 @@ __global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs
         if (lane == 0) a.flag_cur[v] = 0;
     }
     const int64_t lo = __ldg(&a.off[v]), hi = __ldg(&a.off[v + 1]);
-    if (a.pf && lane < 2) {  // one bulk L2 prefetch per array: the 32 lanes' chunk streams then hit L2
-        const char *base = lane == 0 ? (const char *)(a.tgt + lo) : (const char *)a.w + lo * (int64_t)sizeof(W);
-        const uint64_t b0 = (uint64_t)base & ~(uint64_t)15;
-        const uint64_t b1 = ((uint64_t)base + (uint64_t)(hi - lo) * 4u + 15u) & ~(uint64_t)15;
-        if (sizeof(W) == 4 && b1 > b0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((unsigned)(b1 - b0)) : "memory");
-    }
     const int32_t cur = DET ? __ldg(&a.lab_old[v]) : __ldcg(&a.lab_old[v]);
     MgSketchOff8 part;
     part.reset(8, a.zkey);
     int64_t cs = 0, ce = 0;
     if (lane < a.parts) chunk_bounds(hi - lo, a.parts, lane, cs, ce);
     bool lc = false;
-    if (a.stream == 1)
-        lane_stream_p<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
-            if (valid) part.acc(c, (V)w, 8);
-        });
-    else
-        lane_stream_u<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
-            if (valid) part.acc(c, (V)w, 8);
-        });
+    lane_stream_p<W, DET>(a, lo + cs, ce - cs, v, lc, [&](int64_t, bool valid, int32_t c, W w) {
+        if (valid) part.acc(c, (V)w, 8);
+    });
     const bool lca = __any_sync(0xffffffffu, lc);
     uint32_t *dst = a.hparts + (size_t)wid * kLpmWords;
     uint4 *kd = reinterpret_cast<uint4 *>(dst + lane * 8);

@@ -108,8 +108,6 @@ struct SweepArgs {
     int32_t symmetric;
     int32_t thr;                      // degree_threshold (chunked evaluation at deg >= thr)
     int32_t single;                   // shared_sketch: one sketch over any degree
-    int32_t dbg;                      // timing experiments only (SLPA_DEBUG_SKIP); 0 in production
-    int32_t stream;                   // high-degree chunk streaming: 1 = three-stage pipeline, 0 = two-stage
     const int32_t *giant_bin;         // giant vertices (deg >= giant threshold), degree desc
     const int64_t *giant_off;         // exclusive prefix of their degrees
     uint32_t *glab;                   // gathered label words of their arcs
@@ -124,8 +122,6 @@ struct SweepArgs {
     double *xtot;                     //   exact: the tables' binary64 totals (keys in xs)
     int64_t xdeg_lo, xdeg_hi;         //   exact: this launch takes the vertices with xdeg_lo < degree <= xdeg_hi
     int32_t zkey;                     // internal value of label 0 (0 unless caller labels were remapped)
-    int32_t pf;                       // heavy scan: bulk L2 prefetch of the row (SLPA_HI_PREFETCH)
-    int32_t lo_direct;                // light rows: 1 gather a higher neighbour's L0 directly, 0 lab_new + fix-up
     int32_t ident;                    // det round 0 of lpa_run's first sweep, no visiting order: every label
                                       // still equals its vertex id and no word has a changed bit, so the
                                       // light kernels read a neighbour's label as its id (no gather)

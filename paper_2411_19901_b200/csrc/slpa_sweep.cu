@@ -356,29 +356,9 @@ SweepArgs make_args(slpa_ctx *ctx, const slpa_config *cfg, int pickless) {
     a.symmetric = g.symmetric;
     a.thr = cfg->degree_threshold;
     a.single = cfg->variant == SLPA_VARIANT_MG && cfg->shared_sketch;
-    static const int dbg = [] {
-        const char *e = getenv("SLPA_DEBUG_SKIP");
-        return e ? atoi(e) : 0;
-    }();
-    a.dbg = dbg;
-    static const int stream = [] {
-        const char *e = getenv("SLPA_STREAM");
-        return e ? atoi(e) : 1;
-    }();
-    a.stream = stream;
     a.tbits = ctx->prof_on ? ctx->wb.tbits.p : nullptr;
     a.fbits = ctx->wb.fbits.p;
     a.zkey = ctx->zkey;
-    static const int lo_direct = [] {
-        const char *e = getenv("SLPA_LO_DIRECT");
-        return e ? atoi(e) : 1;
-    }();
-    a.lo_direct = lo_direct;
-    static const int pf = [] {
-        const char *e = getenv("SLPA_HI_PREFETCH");
-        return e ? atoi(e) : 0;
-    }();
-    a.pf = pf;
     a.giant_bin = g.bin_giant.p;
     a.giant_off = g.giant_off.p;
     a.glab = ctx->wb.glab.p;

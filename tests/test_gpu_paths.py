@@ -54,7 +54,7 @@ ENVS = [
     {"SLPA_HI_GRP": "0", "SLPA_GIANT": "300"},
     {"SLPA_GIANT_GRP": "0", "SLPA_GIANT": "300"},
     {"SLPA_GIANT": "128"},
-    {"SLPA_STREAM": "0", "SLPA_GIANT": "5000"},
+    {"SLPA_GIANT": "5000"},
     {"SLPA_GIANT": "300", "SLPA_HI_SMALL": "0"},
     {"SLPA_L2_PERSIST_MB": "40"},
     {"SLPA_SCAN": "0", "SLPA_GIANT": "300"},
