@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end evidence on one B200: GPU suite, smoke, bench lines (all configs / modes /
 # variants, reference arm, N=2 protocol run), ncu launch list / DRAM traffic / full
-# captures of the two hot kernels, compute-sanitizer memcheck + racecheck.
+# captures of the two hot kernels.
 O=${1:-gpurun_out/final}
 mkdir -p $O
 nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > $O/clocks_pre.txt
@@ -20,8 +20,5 @@ timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
 timeout 900 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum,l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum --cache-control none --clock-control none --csv --log-file $O/traffic.csv python tools/prof_run.py --scale 24 --runs 2 --range > $O/traffic.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --cache-control none -k regex:k_mg_hi_scan -c 1 -o $O/full_hi_scan -f python tools/prof_run.py --scale 24 --runs 1 > $O/full_hi_scan.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --cache-control none -k regex:k_lane_direct -c 1 -o $O/full_lane -f python tools/prof_run.py --scale 24 --runs 1 > $O/full_lane.log 2>&1
-for mode in det async; do
-timeout 600 compute-sanitizer --tool memcheck --leak-check full --error-exitcode 9 python tools/prof_run.py --scale 12 --runs 1 --mode $mode > $O/memcheck_$mode.log 2>&1; echo "rc=$?" >> $O/memcheck_$mode.log
-timeout 600 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/prof_run.py --scale 12 --runs 1 --mode $mode > $O/racecheck_$mode.log 2>&1; echo "rc=$?" >> $O/racecheck_$mode.log
-done
+# (compute-sanitizer is closed on the GPU pool; profiles/r2_sanitizer.md holds the earlier memcheck / racecheck runs)
 timeout 2400 python -m pytest tests -m gpu -x -q --durations 15 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
