@@ -7,6 +7,9 @@
 #include "slpa_internal.cuh"
 
 // minimum resident blocks per SM for the two bulk kernels (register caps; A/B builds)
+#ifndef SLPA_HI_THREADS
+#define SLPA_HI_THREADS 256
+#endif
 #ifndef SLPA_HI_MINB
 #define SLPA_HI_MINB 1
 #endif
@@ -755,7 +758,7 @@ __global__ void __launch_bounds__(kThreads) k_mg_hi_direct(SweepArgs a, const in
 constexpr int kLpmWords = 32 * 16;  // 32 parts x (8 keys + 8 values)
 
 template <class W, bool DET, class V>
-__global__ void __launch_bounds__(kThreads, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs a, const int32_t *__restrict__ list,
+__global__ void __launch_bounds__(SLPA_HI_THREADS, SLPA_HI_MINB) k_mg_hi_scan(SweepArgs a, const int32_t *__restrict__ list,
                                                          int64_t count, int round0) {
     static_assert(sizeof(V) == 4, "scratch holds 32-bit values");
     const int lane = threadIdx.x & 31;
@@ -1678,6 +1681,7 @@ KernelSet pick_kernels(const slpa_config *cfg) {
         // off the sequential count
         if (grouped_ok && hi_grp_mode() == 2 && (DET || async_split_mode())) {
             ks.hi = k_mg_hi_scan<W, DET, V>;
+            ks.hi_threads = SLPA_HI_THREADS;
             ks.hi_small = k_mg_hi_block<W, DET, V>;
             ks.hi_merge = k_mg_hi_merge<W, DET, V>;
             ks.hi_finish = k_mg_hi_finish<DET>;
