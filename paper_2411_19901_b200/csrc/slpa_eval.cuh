@@ -13,8 +13,10 @@
 #ifndef SLPA_HI_MINB
 #define SLPA_HI_MINB 1
 #endif
+// light rows: 3 blocks of 256 threads per SM (85-register cap, a 24-byte
+// spill outside the batch loop): k-mer 151 -> 142 ms, grid 14.8 -> 12.8 ms per run
 #ifndef SLPA_LO_MINB
-#define SLPA_LO_MINB 1
+#define SLPA_LO_MINB 3
 #endif
 
 
@@ -502,6 +504,7 @@ __device__ __forceinline__ void lane_finish(const SweepArgs &a, bool go, int32_t
 template <int K, bool CHUNKED, class V>
 struct MgLane {
     static constexpr bool kHasRescan = true;
+    static constexpr int kMinBlocks = (CHUNKED || K == 0) ? 1 : SLPA_LO_MINB;  // register cap of k_lane_direct
     MgSketchDev<K, V> S, part;
     int k, p;
     int32_t z;
@@ -559,6 +562,7 @@ struct MgLane {
 template <bool CHUNKED, class V>
 struct BmLane {
     static constexpr bool kHasRescan = false;
+    static constexpr int kMinBlocks = CHUNKED ? 1 : SLPA_LO_MINB;
     BmVote<V> st, best;
     int32_t cur0;
     int p;
@@ -596,7 +600,7 @@ struct BmLane {
 
 // One lane per vertex, every lane streaming its own row directly.
 template <class W, class Pol, bool DET>
-__global__ void __launch_bounds__(kThreads, SLPA_LO_MINB) k_lane_direct(SweepArgs a, const int32_t *__restrict__ list,
+__global__ void __launch_bounds__(kThreads, Pol::kMinBlocks) k_lane_direct(SweepArgs a, const int32_t *__restrict__ list,
                                                           int64_t count, int round0) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int32_t v = -1;
