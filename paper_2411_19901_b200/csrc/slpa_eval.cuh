@@ -7,6 +7,9 @@
 #include "slpa_internal.cuh"
 
 // minimum resident blocks per SM for the two bulk kernels (register caps; A/B builds)
+#ifndef SLPA_MERGE_MINB
+#define SLPA_MERGE_MINB 1
+#endif
 #ifndef SLPA_HI_THREADS
 #define SLPA_HI_THREADS 256
 #endif
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(SLPA_HI_THREADS, SLPA_HI_MINB) k_mg_hi_scan(Sw
 }
 
 template <class W, bool DET, class V>
-__global__ void __launch_bounds__(kThreads) k_mg_hi_merge(SweepArgs a, const int32_t *__restrict__ list,
+__global__ void __launch_bounds__(kThreads, SLPA_MERGE_MINB) k_mg_hi_merge(SweepArgs a, const int32_t *__restrict__ list,
                                                           int64_t count, int) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= count) return;
